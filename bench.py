@@ -1,0 +1,359 @@
+#!/usr/bin/env python3
+"""Benchmark of the quantized-GEMV hot path (BASELINE.json metric, configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (one "step"): one batch-1 qGEMV over each of the 36 distinct weight
+matrices of BASELINE configs[1] — b in {2,3,4} x g in {32,64,128,FC} x KxN in
+{4096x4096, 4096x11008, 11008x4096} — W ~ N(0, 0.02^2) quantized on the GPU
+(bit-exact with the reference), x ~ N(0,1) f32, seeded.  The step reads
+~622 MB of packed weights + scales/zeros, i.e. inputs larger than the 126 MB
+L2, so no L2 flush is needed between steps.
+
+value  = algorithmic bytes (packed codes + f32 scale + f32 zero) of all ranks
+         / device time of the timed steps (max over ranks), GB/s.  The step is
+         a CUDA graph of the 36 kernel launches (programmatic dependent launch
+         between them); inputs are resident in HBM.
+e2e    = same metric through the public API `qgemv(pm, x_host)` with pinned
+         host x in and host y out every call.
+N > 1  = independent replicas of the sweep on every rank (weak scaling, no
+         data-path collective: GEMVs of distinct matrices are independent).
+--impl reference = the reference's CPU path restated by the oracle (C port of
+         the generated kernel, oracle/qgemv_port.c, all host threads).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SWEEP = [(b, g, shp) for shp in [(4096, 4096), (4096, 11008), (11008, 4096)]
+         for b in (2, 3, 4) for g in (32, 64, 128, None)]
+WORKLOAD = ("BASELINE configs[1] sweep: b{2,3,4} x g{32,64,128,full} x KxN"
+            "{4096x4096,4096x11008,11008x4096}, batch 1, f32 activations")
+
+
+def algo_bytes(K, N, bits, g):
+    G = 1 if g is None else K // g
+    return K * N * bits // 8 + G * N * 8
+
+
+STEP_BYTES = sum(algo_bytes(K, N, b, g) for b, g, (K, N) in SWEEP)
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:  # noqa: BLE001
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling via NVML in a thread (SM clock, reasons)."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def report(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference path restated by the oracle (C port, exec layout)
+# ---------------------------------------------------------------------------
+
+def build_cpu_cases(subset):
+    from oracle import qigen_oracle as orc
+    cases = []
+    for i, (b, g, (K, N)) in enumerate(subset):
+        rng = np.random.default_rng(1000 + i)
+        w = rng.normal(0, 0.02, (K, N)).astype(np.float32)
+        codes, s, z = orc.quantize_matrix(w, b, g)
+        mu, tu, m_b, t_b = orc.plan(b, g, (K, N))
+        ex = orc.ExecLayout(orc.pack_rowseq(codes, b), s, z, K, N, b, g, m_b, t_b)
+        x = rng.normal(0, 1, K).astype(np.float32)
+        cases.append((ex, x, algo_bytes(K, N, b, g)))
+    return cases
+
+
+def time_cpu(cases, reps, threads):
+    from oracle import qigen_oracle as orc
+    for ex, x, _ in cases:  # warm-up (2 warm-ups)
+        orc.qgemv_port(ex, x, threads=threads)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for ex, x, _ in cases:
+            orc.qgemv_port(ex, x, threads=threads)
+        times.append(time.perf_counter() - t0)
+    nbytes = sum(c[2] for c in cases)
+    return nbytes / statistics.median(times) / 1e9, statistics.median(times)
+
+
+CPU_SAMPLE = [c for c in SWEEP if c[2] == (4096, 4096)]
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import qigen_oracle as orc
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    cases = build_cpu_cases(CPU_SAMPLE)
+    setup = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        time_cpu(cases, 1, threads)
+    times = []
+    for _ in range(args.steps):
+        _, t = time_cpu(cases, 1, threads)
+        times.append(t)
+    nbytes = sum(c[2] for c in cases)
+    value = nbytes * len(times) / sum(times) / 1e9
+    sample = (f"the 12 4096x4096 matrices of the sweep (b x g), {nbytes / 1e6:.1f} MB per step; "
+              f"C port of the reference's generated kernel on its exec layout, {threads} threads "
+              f"(setup {setup:.1f} s untimed)")
+    line = {"metric": "quantized GEMV effective HBM GB/s", "value": round(value, 4), "unit": "GB/s",
+            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "sample": "4096x4096 slice"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    _ = orc
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2307_03738_b200 as q
+    from paper_2307_03738_b200.runtime import PanelWeights
+
+    dev = torch.device("cuda", local)
+    mats, xs, ys, pms = [], [], [], []
+    gen = torch.Generator(device=dev)
+    for i, (b, g, (K, N)) in enumerate(SWEEP):
+        gen.manual_seed(1000 + i + 7919 * rank)
+        w = torch.randn((K, N), generator=gen, device=dev) * 0.02
+        cfg = q.QuantConfig(b, g)
+        cm = q.quantize_matrix(w, cfg)
+        # the reference-format object a user holds, and its GPU layout cache
+        pm = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cfg, (K, N)))
+        pw = q.runtime.exec_layout(pm)
+        del w, cm
+        mats.append(pw)
+        pms.append(pm)
+        xs.append(torch.randn(K, generator=gen, device=dev))
+        ys.append(torch.empty(N, device=dev))
+    # drop the reference-format words (keep only the GPU layout in HBM)
+    for pm in pms:
+        pm.words = pm.words[:0]
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for pw, x, y in zip(mats, xs, ys):
+            pw.gemv(x, out=y)
+
+    with torch.cuda.stream(stream):
+        step()
+        stream.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+    stream.synchronize()
+
+    sampler = ClockSampler(local)
+    with sampler:
+        with torch.cuda.stream(stream):
+            # warm-up (+ a short soak so the clock sampler sees the GPU under load)
+            soak_end = time.perf_counter() + 0.5
+            w_done = 0
+            while w_done < args.warmup or time.perf_counter() < soak_end:
+                graph.replay()
+                w_done += 1
+                if w_done % 50 == 0:
+                    stream.synchronize()
+            stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            e1.record(stream)
+            e1.synchronize()
+            torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_per_step = ms / args.steps
+    value = STEP_BYTES * world * args.steps / (ms / 1e3) / 1e9
+    kernel_gbs = STEP_BYTES / (ms_per_step / 1e3) / 1e9
+
+    # --- e2e through the public API with host buffers --------------------------
+    xs_host = [x.cpu().pin_memory() for x in xs]
+    e2e_steps = max(1, min(args.steps, 20))
+    for pm, xh in zip(pms, xs_host):  # warm-up
+        q.qgemv(pm, xh)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for pm, xh in zip(pms, xs_host):
+            q.qgemv(pm, xh)  # H2D x, kernel, D2H y (blocking, returns a host tensor)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = STEP_BYTES * world * e2e_steps / e2e_s / 1e9
+    h2d = sum(K * 4 for _, _, (K, N) in SWEEP)
+    d2h = sum(N * 4 for _, _, (K, N) in SWEEP)
+
+    if rank == 0:
+        peak, peak_src = measured_peak()
+        line = {
+            "metric": "quantized GEMV effective HBM GB/s",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8 x s8 -> s32 (IMMA), f32 epilogue",
+            "data": "synthetic (seeded N(0,0.02^2) weights, N(0,1) activations)",
+            "config": {"workload": WORKLOAD, "matrices": len(SWEEP),
+                       "bytes_per_step": STEP_BYTES,
+                       "l2": "inputs larger than L2 (%.0f MB per step vs 126 MB)" % (STEP_BYTES / 1e6),
+                       "launch": "CUDA graph of 36 launches, PDL", "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "hbm", "achieved": round(kernel_gbs, 1), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s",
+                         "frac": round(kernel_gbs / peak, 4), "traffic": _traffic()},
+            "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+            "gpu_launches": len(SWEEP) * args.steps,
+            "clocks": sampler.report(),
+        }
+        if not args.no_cpu_baseline:
+            threads = len(os.sched_getaffinity(0))
+            cases = build_cpu_cases(CPU_SAMPLE)
+            gbs, _ = time_cpu(cases, 3, threads)
+            line["cpu_baseline"] = {
+                "value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                "sample": "12 4096x4096 matrices of the sweep, median of 3 passes, C port of the "
+                          "reference's generated kernel (oracle/qgemv_port.c)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _traffic():
+    """DRAM bytes per step from the committed ncu summary, if one exists."""
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_step")
+        except Exception:  # noqa: BLE001
+            return None
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,134 @@
+/* qigen_b200.h — C ABI of libqigen_b200.so, the B200 (sm_100a) implementation
+ * of QIGen's quantized-GEMV hot path (arXiv 2307.03738).
+ *
+ * Plain pointers and sizes only.  Every pointer argument is a DEVICE pointer
+ * unless its name ends in `_host`.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Every call is stream-ordered and returns a qigen_status;
+ * on failure qigen_last_error() returns a message.  Status codes map onto the
+ * reference's exception classes (config.py:34 ConfigError, packing.py:35
+ * PackError, perfmodel.py:20 PlanError, all ValueError subclasses).
+ *
+ * Orientation follows the reference: W is n x m (n = K input
+ * rows, m = N output columns), groups run along n per column, y = x W.
+ *
+ * Which reference interface each entry point replaces is cited on it; the
+ * reference has no native FFI of its own — its seam is the runtime op
+ * qgemv(pm, x, sums, threads) and the generated-kernel
+ * calling convention (kernelgen.py:399-401).  INTEGRATION.md shows the
+ * ctypes binding a maintainer of the reference would add.
+ */
+#ifndef QIGEN_B200_H_
+#define QIGEN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QIGEN_OK = 0,
+  QIGEN_ERR_CONFIG = 1,      /* ConfigError  (config.py:34)  */
+  QIGEN_ERR_PACK = 2,        /* PackError    (packing.py:35) */
+  QIGEN_ERR_PLAN = 3,        /* PlanError    (perfmodel.py:20) */
+  QIGEN_ERR_CUDA = 4,        /* CUDA runtime failure          */
+  QIGEN_ERR_ARG = 5,         /* null pointer / bad size       */
+  QIGEN_ERR_UNSUPPORTED = 6  /* combination not implemented   */
+} qigen_status;
+
+typedef enum { QIGEN_ZERO_REAL32 = 0, QIGEN_ZERO_QUANTIZED = 1 } qigen_zero_mode; /* config.py:17-31 */
+typedef enum { QIGEN_LAYOUT_ROW_SEQUENTIAL = 0, QIGEN_LAYOUT_ZCURVE = 1 } qigen_layout; /* packing.py:30-32 */
+typedef enum { QIGEN_F32 = 0, QIGEN_F16 = 1, QIGEN_BF16 = 2 } qigen_dtype;
+
+int qigen_version(void);
+const char* qigen_last_error(void);
+
+/* ---- quantization (bit-exact with quant.py) ------------------------------- */
+
+/* quant.py:119-127 quantize_matrix (+ _quantize_blocks :74-94).
+ * w: f32 [n, m] row-major.  group_size 0 = FULL_COLUMN (config.py:12).
+ * codes: u8 [n, m]; scales, zeros: f32 [G, m], G = n/group_size (1 for FC). */
+int qigen_quantize(const float* w, int64_t n, int64_t m, int bits, int64_t group_size,
+                   int zero_mode, uint8_t* codes, float* scales, float* zeros, void* stream);
+
+/* quant.py:130-138 dequantize_matrix: out[n, m] = f32(s * (f32(code) - z)). */
+int qigen_dequantize(const uint8_t* codes, const float* scales, const float* zeros,
+                     int64_t n, int64_t m, int64_t group_size, float* out, void* stream);
+
+/* ---- packing (bit-exact with packing.py) ---------------------------------- */
+
+/* packing.py:204-214 _pack_matrix_rowseq: codes [n, m] -> n*m*bits/32 words,
+ * word (r, k, c) at (r*Kw + k)*m + c (Kw = 3 for 3-bit, else 1). */
+int qigen_pack_rowseq(const uint8_t* codes, int64_t n, int64_t m, int bits, uint32_t* words,
+                      void* stream);
+/* packing.py:229-242 extract_codes (ROW_SEQUENTIAL part): words -> codes [n, m]. */
+int qigen_unpack_rowseq(const uint32_t* words, int64_t n, int64_t m, int bits, uint8_t* codes,
+                        void* stream);
+/* packing.py:175-201 _storage_permutation applied to words.  blk_rc holds the
+ * (row_block, col_block) pairs in Morton storage order (packing.py:110-114),
+ * int32 [nblk * 2], device memory.  to_zcurve=1: rowseq -> zcurve, 0: inverse. */
+int qigen_permute_zcurve(const uint32_t* src, uint32_t* dst, int64_t n, int64_t m, int bits,
+                         int64_t m_b, int64_t t_b, const int32_t* blk_rc, int64_t nblk,
+                         int to_zcurve, void* stream);
+
+/* ---- GPU panel layout --------------------------------------- */
+
+/* Sizes of the panel layout: uint32 words of packed codes and float2 (s, z)
+ * pairs.  K is padded to a multiple of 256 and m to a multiple of 16. */
+int64_t qigen_panel_words(int64_t n, int64_t m, int bits);
+int64_t qigen_panel_params(int64_t n, int64_t m, int64_t group_size);
+
+/* Re-tile codes + scales/zeros into the panel layout (qw, qsz). */
+int qigen_panels_from_codes(const uint8_t* codes, const float* scales, const float* zeros,
+                            int64_t n, int64_t m, int bits, int64_t group_size, uint32_t* qw,
+                            float* qsz, void* stream);
+/* Inverse of the code part (round-trip tests). */
+int qigen_panels_to_codes(const uint32_t* qw, int64_t n, int64_t m, int bits, uint8_t* codes,
+                          void* stream);
+/* Re-tile directly from reference ROW_SEQUENTIAL words (3-bit straddles of the
+ * 96-bit stream, kernelgen.py:116-124, are resolved here). */
+int qigen_panels_from_rowseq(const uint32_t* words, const float* scales, const float* zeros,
+                             int64_t n, int64_t m, int bits, int64_t group_size, uint32_t* qw,
+                             float* qsz, void* stream);
+
+/* ---- the hot path ----------------------------------------------------------- */
+
+/* Per-group input sums (Eq. 2): out[G] (FC: out[0] = total).
+ * fp64 accumulation, rounded once to f32. */
+int qigen_input_sums(const float* x, int64_t n, int64_t group_size, float* out, void* stream);
+
+/* Replaces qgemv(pm, x, sums, threads) and the generated
+ * kernel it drives (kernelgen.py:371-423).  x: `tokens` rows of n activations
+ * (dtype x_dtype, row stride ldx elements); y: f32 [tokens, m] with row stride
+ * ldy.  accumulate=0 overwrites y, 1 adds to it.  k_splits=0 picks the K split
+ * automatically.  Deterministic: results do not depend on the launch shape
+ * beyond (n, m, bits, group_size, tokens, k_splits).  Input sums are fused. */
+int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+               int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
+               float* y, int64_t ldy, int accumulate, int k_splits, void* stream);
+
+/* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
+
+typedef struct qigen_weights qigen_weights;
+
+/* Build a device-resident weight handle from reference-format device buffers:
+ * packed words in `layout` (ZCURVE needs blk_rc/nblk/m_b/t_b, else pass 0),
+ * scales/zeros f32 [G, m]. */
+int qigen_weights_create(const uint32_t* words, int layout, int64_t n, int64_t m, int bits,
+                         int64_t group_size, int64_t m_b, int64_t t_b, const int32_t* blk_rc,
+                         int64_t nblk, const float* scales, const float* zeros, void* stream,
+                         qigen_weights** out);
+int qigen_weights_destroy(qigen_weights* w);
+/* qgemv on device buffers through the handle. */
+int qigen_weights_gemv(const qigen_weights* w, const void* x, int x_dtype, int64_t tokens,
+                       float* y, int accumulate, void* stream);
+/* End-to-end call with HOST buffers: copies x_host in, runs the GEMV, copies
+ * y_host out and synchronises `stream` (the reference-facing blocking call). */
+int qigen_weights_gemv_host(const qigen_weights* w, const float* x_host, int64_t tokens,
+                            float* y_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QIGEN_B200_H_ */

@@ -1,0 +1,99 @@
+"""ctypes binding of libqigen_b200.so (include/qigen_b200.h).
+
+The library is the only compute path: if it is missing or no CUDA device is
+present, every op raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .config import ConfigError
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("QIGEN_B200_LIB", _HERE / "libqigen_b200.so"))
+
+OK, ERR_CONFIG, ERR_PACK, ERR_PLAN, ERR_CUDA, ERR_ARG, ERR_UNSUPPORTED = range(7)
+F32, F16, BF16 = 0, 1, 2
+
+
+class QigenCudaError(RuntimeError):
+    """A CUDA runtime failure inside libqigen_b200."""
+
+
+class UnsupportedError(ValueError):
+    """The combination is valid for the reference but not implemented here."""
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "qigen_version": (_I32, []),
+    "qigen_last_error": (ctypes.c_char_p, []),
+    "qigen_quantize": (_I32, [_P, _I64, _I64, _I32, _I64, _I32, _P, _P, _P, _P]),
+    "qigen_dequantize": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P]),
+    "qigen_pack_rowseq": (_I32, [_P, _I64, _I64, _I32, _P, _P]),
+    "qigen_unpack_rowseq": (_I32, [_P, _I64, _I64, _I32, _P, _P]),
+    "qigen_permute_zcurve": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _I64, _P, _I64, _I32, _P]),
+    "qigen_panel_words": (_I64, [_I64, _I64, _I32]),
+    "qigen_panel_params": (_I64, [_I64, _I64, _I64]),
+    "qigen_panels_from_codes": (_I32, [_P, _P, _P, _I64, _I64, _I32, _I64, _P, _P, _P]),
+    "qigen_panels_to_codes": (_I32, [_P, _I64, _I64, _I32, _P, _P]),
+    "qigen_panels_from_rowseq": (_I32, [_P, _P, _P, _I64, _I64, _I32, _I64, _P, _P, _P]),
+    "qigen_input_sums": (_I32, [_P, _I64, _I64, _P, _P]),
+    "qigen_gemv": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64,
+                          _I32, _I32, _P]),
+    "qigen_weights_create": (_I32, [_P, _I32, _I64, _I64, _I32, _I64, _I64, _I64, _P, _I64,
+                                    _P, _P, _P, ctypes.POINTER(_P)]),
+    "qigen_weights_destroy": (_I32, [_P]),
+    "qigen_weights_gemv": (_I32, [_P, _P, _I32, _I64, _P, _I32, _P]),
+    "qigen_weights_gemv_host": (_I32, [_P, _P, _I64, _P, _P]),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(status: int) -> None:
+    """Map a qigen_status onto the reference's exception classes."""
+    if status == OK:
+        return
+    msg = lib().qigen_last_error().decode(errors="replace")
+    if status == ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == ERR_PACK:
+        from .packing import PackError
+        raise PackError(msg)
+    if status == ERR_PLAN:
+        from .perfmodel import PlanError
+        raise PlanError(msg)
+    if status == ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    if status == ERR_CUDA:
+        raise QigenCudaError(msg)
+    raise ValueError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))

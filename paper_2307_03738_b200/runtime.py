@@ -1,0 +1,241 @@
+"""Runtime: the quantized GEMV behind the reference's seam.
+
+The reference declares a runtime it never shipped:
+``input_sums``, ``qgemv_reference``, ``qgemv(pm, x, sums, threads)`` and
+``memory_report``.  This module provides them with the same argument meaning
+and errors, backed by libqigen_b200:
+
+* ``qgemv`` accepts any ``PackedMatrix`` (ours or the reference's, either
+  ``Layout``).  The first call re-tiles it into the GPU panel layout
+   and caches it in ``pm._exec_cache`` — the reference's own hook
+  (packing.py:135).  Input sums are fused into the kernel, so ``sums`` is
+  accepted for API compatibility and ignored; ``threads`` (CPU column-block
+  threads) has no GPU meaning and is only validated.
+* numpy in -> numpy out (host round trip, like the reference); CUDA tensor in ->
+  CUDA tensor out (stream-ordered, no host sync).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev
+from ._lib import BF16, F16, F32, call, lib
+from .config import ConfigError, QuantConfig
+from .packing import Layout, PackError, _as_config, _as_words, rowseq_words
+from .quant import CodeMatrix, quantize_matrix
+
+_DTYPES = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
+MAX_GEMV_TOKENS = 16
+
+
+@dataclass
+class InputSums:
+    """total x-hat and per-group sums."""
+
+    total: float
+    per_group: torch.Tensor
+
+
+def input_sums(x, group_size) -> InputSums:
+    """SPEC.md:331-339 on the GPU (fp64 accumulation, one rounding)."""
+    xt = _dev.to_device(x, torch.float32)
+    if xt.dim() != 1 or xt.numel() == 0:
+        raise ConfigError(f"x must be a non-empty vector, got shape {tuple(xt.shape)}")
+    n = xt.numel()
+    if group_size is not None and n % group_size:
+        raise ConfigError(f"group size {group_size} does not divide length {n}")
+    G = 1 if group_size is None else n // group_size
+    per = torch.empty(G, dtype=torch.float32, device=xt.device)
+    tot = torch.empty(1, dtype=torch.float32, device=xt.device)
+    st = _dev.stream_handle()
+    call("qigen_input_sums", xt.data_ptr(), n, 0 if group_size is None else group_size,
+         per.data_ptr(), st)
+    call("qigen_input_sums", xt.data_ptr(), n, 0, tot.data_ptr(), st)
+    return InputSums(float(tot.item()), per)
+
+
+class PanelWeights:
+    """A weight matrix in the GPU panel layout.
+
+    ``qw``: packed codes, 16-column panels x 256-row supersteps, each lane's
+    128-bit words holding whole m16n8k32 A fragments; ``qsz``: (s, z) float2 per
+    (panel, group, column).  Built from codes, reference words, or float
+    weights (GPU quantize, bit-exact with quant.py)."""
+
+    def __init__(self, qw: torch.Tensor, qsz: torch.Tensor, n: int, m: int, config: QuantConfig):
+        self.qw, self.qsz = qw, qsz
+        self.n, self.m, self.config = n, m, config
+
+    @property
+    def bits(self) -> int:
+        return self.config.bits
+
+    @property
+    def group_code(self) -> int:
+        return self.config.group_code
+
+    @staticmethod
+    def _alloc(n, m, config, device):
+        L = lib()
+        qw = torch.empty(int(L.qigen_panel_words(n, m, config.bits)), dtype=torch.int32, device=device)
+        qsz = torch.empty(int(L.qigen_panel_params(n, m, config.group_code)) * 2,
+                          dtype=torch.float32, device=device)
+        return qw, qsz
+
+    @classmethod
+    def from_codes(cls, cm: CodeMatrix) -> "PanelWeights":
+        cfg = _as_config(cm.config)
+        codes = _dev.to_device(cm.codes, torch.uint8)
+        s = _dev.to_device(cm.scales, torch.float32)
+        z = _dev.to_device(cm.zeros, torch.float32)
+        n, m = codes.shape
+        qw, qsz = cls._alloc(n, m, cfg, codes.device)
+        call("qigen_panels_from_codes", codes.data_ptr(), s.data_ptr(), z.data_ptr(), n, m,
+             cfg.bits, cfg.group_code, qw.data_ptr(), qsz.data_ptr(), _dev.stream_handle())
+        return cls(qw, qsz, n, m, cfg)
+
+    @classmethod
+    def from_packed(cls, pm) -> "PanelWeights":
+        """From a reference-format PackedMatrix (ROW_SEQUENTIAL or ZCURVE words)."""
+        cfg = _as_config(pm.config)
+        rs = rowseq_words(pm)
+        s = _dev.to_device(pm.scales, torch.float32)
+        z = _dev.to_device(pm.zeros, torch.float32)
+        G = cfg.groups_for_rows(pm.n)
+        if tuple(s.shape) != (G, pm.m) or tuple(z.shape) != (G, pm.m):
+            raise PackError(f"scales/zeros shape {tuple(s.shape)} != ({G}, {pm.m})")
+        qw, qsz = cls._alloc(pm.n, pm.m, cfg, rs.device)
+        call("qigen_panels_from_rowseq", rs.data_ptr(), s.data_ptr(), z.data_ptr(), pm.n, pm.m,
+             cfg.bits, cfg.group_code, qw.data_ptr(), qsz.data_ptr(), _dev.stream_handle())
+        return cls(qw, qsz, pm.n, pm.m, cfg)
+
+    @classmethod
+    def from_float(cls, w, config: QuantConfig) -> "PanelWeights":
+        """Quantize float weights [n, m] on the GPU and re-tile (no host copy)."""
+        cm = quantize_matrix(w, config)
+        out = cls.from_codes(cm)
+        del cm
+        return out
+
+    def to_codes(self) -> torch.Tensor:
+        codes = torch.empty((self.n, self.m), dtype=torch.uint8, device=self.qw.device)
+        call("qigen_panels_to_codes", self.qw.data_ptr(), self.n, self.m, self.bits,
+             codes.data_ptr(), _dev.stream_handle())
+        return codes
+
+    def nbytes_algorithmic(self) -> int:
+        """Packed codes + f32 scale + f32 zero (the roofline bytes)."""
+        G = self.config.groups_for_rows(self.n)
+        return self.n * self.m * self.bits // 8 + G * self.m * 8
+
+    def gemv(self, x: torch.Tensor, out: torch.Tensor | None = None, *, accumulate: bool = False,
+             k_splits: int = 0) -> torch.Tensor:
+        """y[t, :] = x[t, :] @ W for t < tokens; x: CUDA [tokens, n] or [n]."""
+        squeeze = x.dim() == 1
+        x2 = x.reshape(1, -1) if squeeze else x
+        if x2.dim() != 2 or x2.shape[1] != self.n:
+            raise ConfigError(f"x has shape {tuple(x.shape)}, expected [..., {self.n}]")
+        if x2.dtype not in _DTYPES:
+            x2 = x2.float()
+        if x2.stride(1) != 1:
+            x2 = x2.contiguous()
+        T = x2.shape[0]
+        if out is None:
+            out = torch.empty((T, self.m), dtype=torch.float32, device=x2.device)
+            accumulate = False
+        y2 = out.reshape(T, self.m) if out.dim() == 1 else out
+        if y2.dtype != torch.float32 or y2.stride(1) != 1:
+            raise ConfigError("out must be float32 with unit column stride")
+        st = _dev.stream_handle()
+        for t0 in range(0, T, MAX_GEMV_TOKENS):
+            t1 = min(T, t0 + MAX_GEMV_TOKENS)
+            xs, ys = x2[t0:t1], y2[t0:t1]
+            call("qigen_gemv", self.qw.data_ptr(), self.qsz.data_ptr(), self.n, self.m, self.bits,
+                 self.group_code, xs.data_ptr(), _DTYPES[xs.dtype], t1 - t0, xs.stride(0),
+                 ys.data_ptr(), ys.stride(0), int(accumulate), int(k_splits), st)
+        return out.reshape(self.m) if squeeze else out
+
+
+def exec_layout(pm) -> PanelWeights:
+    """The cached GPU layout of a PackedMatrix (packing.py:135 hook)."""
+    cache = getattr(pm, "_exec_cache", None)
+    if isinstance(cache, PanelWeights) and cache.qw.device.index == torch.cuda.current_device():
+        return cache
+    pw = PanelWeights.from_packed(pm)
+    try:
+        pm._exec_cache = pw
+    except AttributeError:
+        pass
+    return pw
+
+
+def qgemv(pm, x, sums=None, threads=None, *, out=None, accumulate: bool = False):
+    """y = x W through the GPU kernel.
+
+    ``x``: [n] or [tokens, n] (numpy, or CUDA tensor in f32/f16/bf16).
+    Returns numpy for host input, a CUDA f32 tensor for device input.
+    """
+    if threads is not None and (not isinstance(threads, (int, np.integer)) or threads < 1):
+        raise ConfigError(f"thread count must be >= 1, got {threads!r}")
+    host = _dev.is_host(x)
+    if isinstance(x, torch.Tensor) and host:
+        # CPU torch tensor (possibly pinned): async H2D, result returned as a CPU tensor
+        if x.shape[-1] != pm.n or x.dim() not in (1, 2):
+            raise ConfigError(f"x has shape {tuple(x.shape)}, expected [..., {pm.n}]")
+        xt = x.to(device=_dev.require_cuda(), dtype=torch.float32, non_blocking=True)
+        y = exec_layout(pm).gemv(xt)
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y.cpu()
+    if host:
+        xa = np.asarray(x, dtype=np.float32)
+        if xa.ndim not in (1, 2) or xa.shape[-1] != pm.n:
+            raise ConfigError(f"x has shape {xa.shape}, expected [{pm.n}] or [tokens, {pm.n}]")
+        if not np.all(np.isfinite(xa)):
+            raise ConfigError("x contains non-finite values")
+        xt = _dev.to_device(xa, torch.float32)
+    else:
+        xt = x
+        if xt.shape[-1] != pm.n or xt.dim() not in (1, 2):
+            raise ConfigError(f"x has shape {tuple(xt.shape)}, expected [..., {pm.n}]")
+    pw = exec_layout(pm)
+    squeeze = xt.dim() == 1
+    x2 = xt.reshape(1, -1) if squeeze else xt
+    y = pw.gemv(x2, out=None if host or out is None else out.reshape(x2.shape[0], pm.m),
+                accumulate=accumulate and out is not None)
+    if squeeze:
+        y = y.reshape(pm.m)
+    if host:
+        yh = _dev.to_host(y)
+        if out is not None:
+            np.copyto(out, yh)
+            return out
+        return yh
+    return y
+
+
+def qgemv_reference(pm, x):
+    """the unfactored dense oracle, on the GPU — full
+    dequantization (quant.py:130-138) then an fp64 matrix product."""
+    from .packing import extract_codes
+    from .quant import dequantize_matrix
+    host = _dev.is_host(x)
+    xt = _dev.to_device(x, torch.float64)
+    if xt.shape[-1] != pm.n:
+        raise ConfigError(f"dimension mismatch: x has {xt.shape[-1]} entries, W has {pm.n} rows")
+    wd = dequantize_matrix(extract_codes(pm)).double()
+    y = xt @ wd
+    return _dev.to_host(y) if host else y
+
+
+def memory_report(pm) -> dict:
+    """payload decomposition and compression vs. 32 n m."""
+    wb, sb, zb = pm.payload_bits()
+    total = wb + sb + zb
+    return {"weight_bits": wb, "scale_bits": sb, "zero_bits": zb, "total_bits": total,
+            "fp32_bits": 32 * pm.n * pm.m, "ratio": 32 * pm.n * pm.m / total}

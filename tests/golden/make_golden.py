@@ -92,6 +92,13 @@ def main() -> None:
                     if m > 3:
                         w[:, 2] = np.tile(np.array([0.0, 0.5, 3.0, 1.5], np.float32), n // 4)
                         w[: n // 2, 3] = -0.0
+                    if m > 5:  # min is a signed zero: the last of +0/-0 decides z's sign
+                        w[:, 4] = np.abs(w[:, 4])
+                        w[::5, 4] = 0.0
+                        w[::7, 4] = -0.0
+                        w[:, 5] = -np.abs(w[:, 5])
+                        w[1::3, 5] = -0.0
+                        w[2::5, 5] = 0.0
                     cm = quant.quantize_matrix(w, QuantConfig(bits, g, zm))
                     unit = qcfg.pack_unit(bits)[0]
                     m_b = 3 * (unit if g is None else int(np.lcm(unit, g)))
