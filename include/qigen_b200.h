@@ -108,6 +108,14 @@ int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int b
                int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
                float* y, int64_t ldy, int accumulate, int k_splits, void* stream);
 
+/* Debugging aid: when buf is non-NULL every later qigen_gemv launch writes
+ * %globaltimer stamps (entry, after the PDL wait, after the activation
+ * prologue, after the main loop, exit) to buf[(cta_y*grid_x + cta_x)*8 + i]. */
+int qigen_debug_trace(void* buf);
+/* Tuning aid: weight stages per warp issued before griddepcontrol.wait
+ * (-1 = the whole first ring fill, the default). */
+int qigen_debug_prefetch(int stages_before_wait);
+
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
 
 typedef struct qigen_weights qigen_weights;

@@ -6,7 +6,7 @@
 //     y_j = sum_g s_gj * ( sum_{i in g} x_i c_ij  -  z_gj * X_g )
 // but the inner product sum x_i c_ij is computed EXACTLY on the integer tensor
 // cores (IMMA, mma.sync.m16n8k32.u8.s8):
-//   * codes c (0..2^b-1) are the u8 A operand, unpacked from the panel layout
+//   * codes c (0..2^b-1) are the u8 A operand, rebuilt from the panel layout
 //     with one or two shift/LOP3 per 4 codes (no int->float conversion);
 //   * each activation row x (f32/f16/bf16) is converted per CTA K-chunk to a
 //     fixed-point integer m = rint(x * 2^(30-E)), |m| < 2^30, split into four
@@ -14,11 +14,17 @@
 //     digits are the s8 B operand, one n8 column per (token, digit);
 //   * the int32 accumulators are exact; at every quantisation-group boundary
 //     they are folded into f32 with the scale/zero correction (the flush).
-// One warp owns a 16-column panel over the CTA's K-chunk; CTAs that share a
-// panel group but own different K-chunks form a thread-block cluster and reduce
-// their partial outputs through distributed shared memory in a fixed order
-// (deterministic, no atomics, no workspace).  Programmatic dependent launch:
-// weights are prefetched before griddepcontrol.wait, activations after it.
+//
+// Data movement: one warp owns a 16-column panel over the CTA's
+// K-chunk and streams it through its own ring of shared-memory stages filled
+// by 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx); a stage is
+// one 256-row superstep of codes plus, for g | 256, the (s, z) pairs of the
+// groups it closes.  The first ring fill is issued BEFORE griddepcontrol.wait,
+// so under programmatic dependent launch the weight stream of this GEMV
+// overlaps the tail of the previous kernel.  CTAs sharing panels but owning
+// different K-chunks form a thread-block cluster and reduce their partial
+// outputs through distributed shared memory in a fixed order (deterministic,
+// no atomics, no workspace).
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -40,17 +46,52 @@ struct GemvArgs {
   int KS, P, Gp, g;  // g = group size; 0 = full column
   int M;             // tokens
   int x_dtype;
+  int x_vec;         // x rows 16-byte aligned -> vector loads
   int accumulate;
-  int max_steps;     // max K-steps of any chunk (smem sizing)
-  int max_ranges;    // max flush ranges of any chunk
+  int max_steps;     // max K-steps (32 rows) of any chunk
+  int D;             // ring stages per warp
+  int pre;           // stages per warp issued before griddepcontrol.wait
+  unsigned long long* trace;  // optional per-CTA timestamps (qigen_debug_trace)
 };
 
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
+__device__ __forceinline__ void trace_point(const GemvArgs& a, int i) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = t;
+  }
+}
+
+// ---- PTX helpers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint2 b) {
@@ -59,12 +100,6 @@ __device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint2 
       "{%0,%1,%2,%3};"
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
-}
-
-__device__ __forceinline__ float load_x(const void* x, int dtype, int64_t idx) {
-  if (dtype == QIGEN_F32) return __ldg((const float*)x + idx);
-  if (dtype == QIGEN_F16) return __half2float(((const __half*)x)[idx]);
-  return __bfloat162float(((const __nv_bfloat16*)x)[idx]);
 }
 
 // Fragment registers of local step sl (0..7) from the lane's superstep words.
@@ -117,25 +152,70 @@ __device__ __forceinline__ void extract<3>(const uint4 (&w)[3], int sl, uint32_t
 
 __device__ __forceinline__ int sbyte(int v) { return (int)(int8_t)(v & 0xFF); }
 
+// Four consecutive activations as f32 (zero beyond n).
+__device__ __forceinline__ void load_x4(const GemvArgs& a, int tk, int64_t k, float (&v)[4]) {
+  const int64_t base = tk * a.ldx + k;
+  if (a.x_vec && k + 3 < a.n) {
+    if (a.x_dtype == QIGEN_F32) {
+      const float4 f = __ldg((const float4*)((const float*)a.x + base));
+      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    } else {
+      const uint2 u = __ldg((const uint2*)((const uint16_t*)a.x + base));
+      if (a.x_dtype == QIGEN_F16) {
+        const float2 lo = __half22float2(*(const __half2*)&u.x), hi = __half22float2(*(const __half2*)&u.y);
+        v[0] = lo.x; v[1] = lo.y; v[2] = hi.x; v[3] = hi.y;
+      } else {
+        const float2 lo = __bfloat1622float2(*(const __nv_bfloat162*)&u.x);
+        const float2 hi = __bfloat1622float2(*(const __nv_bfloat162*)&u.y);
+        v[0] = lo.x; v[1] = lo.y; v[2] = hi.x; v[3] = hi.y;
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float f = 0.f;
+    if (k + i < a.n) {
+      if (a.x_dtype == QIGEN_F32) f = __ldg((const float*)a.x + base + i);
+      else if (a.x_dtype == QIGEN_F16) f = __half2float(((const __half*)a.x)[base + i]);
+      else f = __bfloat162float(((const __nv_bfloat16*)a.x)[base + i]);
+    }
+    v[i] = f;
+  }
+}
+
 // Shared-memory carve-up (bytes), identical on host and device.
 struct SmemLayout {
-  int bfrag, xstep, xr, yp, expo, red, total;
-  __host__ __device__ SmemLayout(int max_steps, int NB, int M, int max_ranges, int WPC) {
+  int ring, bars, bfrag, xu, su, zero, yp, total, stage;
+  __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int M, int WPC, int S) {
+    stage = bits * 512 + szb;
+    const int max_units = max_steps;  // units are >= 32 rows
     int off = 0;
-    bfrag = off; off += max_steps * NB * 32 * 8;
-    xstep = off; off += max_steps * M * 8;
-    xr = off;    off += max_ranges * M * 4;
-    yp = off;    off += WPC * 16 * M * 4;
-    expo = off;  off += 16 * 4;
-    red = off;   off += 32 * 16 * 4;
+    ring = off;  off += WPC * D * stage;
+    bars = off;  off += WPC * D * 8;
+    bfrag = off; off += max_steps * M * 128;
+    xu = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
+    su = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
+    zero = off;  off += 16;
+    yp = off;    off += ((WPC * 16 * M + S - 1) / S) * S * 4 + 16;
     total = off;
   }
 };
 
-template <int BITS, int NB, int WPC, int D>
-__global__ void __launch_bounds__(WPC * 32) gemv_kernel(const GemvArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// GPS = quantisation groups closed per superstep: 8, 4, 2, 1 for g = 32, 64,
+// 128, 256 (their (s, z) ride in the stage), 0 for longer groups (g a multiple
+// of 256 or full column; (s, z) prefetched from global one group ahead).
+// Exponent/flush unit U = min(g, 128) rows: the activations of one unit share a
+// fixed-point exponent (found with warp shuffles, no CTA barrier), and the
+// integer accumulators are folded into f32 once per unit.
+template <int BITS, int NB, int WPC, int GPS>
+__global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
   constexpr int T = WPC * 32;
+  constexpr int SZB = GPS * 128;
+  constexpr int UPS = GPS > 2 ? GPS : 2;   // flush units per superstep
+  constexpr int SPU = 8 / UPS;             // steps per unit
+  constexpr int IPU = SPU * 8;             // prologue items (4 rows) per unit
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const int S = gridDim.y, ys = blockIdx.y;
@@ -143,236 +223,323 @@ __global__ void __launch_bounds__(WPC * 32) gemv_kernel(const GemvArgs a) {
   const int nks = ks1 - ks0;
   const int p = blockIdx.x * WPC + warp;
   const bool active = p < a.P;
-  const int M = a.M;
-  SmemLayout L(a.max_steps, NB, M, a.max_ranges, WPC);
-  uint2* bfrag = (uint2*)(smem + L.bfrag);
-  double* xstep = (double*)(smem + L.xstep);
-  float* xr = (float*)(smem + L.xr);
-  float* yp = (float*)(smem + L.yp);
-  int* expo = (int*)(smem + L.expo);
-  float* red = (float*)(smem + L.red);
-
-  // ---- 1. weight prefetch (independent of the previous kernel) -------------
-  const uint4* wp = a.qw + ((int64_t)(active ? p : 0) * a.KS + ks0) * BITS * 32 + lane;
-  uint4 buf[D][BITS];
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-#pragma unroll
-    for (int v = 0; v < BITS; ++v)
-      buf[d][v] = (active && d < nks) ? ldg_stream(wp + (d * BITS + v) * 32) : make_uint4(0, 0, 0, 0);
-
-  // ---- 2. PDL: wait for the producer of x; let our successor start early ---
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
-
-  // ---- 3. activation prologue: fixed-point digits + range sums -------------
-  const int64_t k0 = (int64_t)ks0 * kSuper;
+  const int M = a.M, D = a.D;
   const int nsteps = nks * 8;
-  const int64_t kend = min((int64_t)ks1 * kSuper, a.n);
+  const int nunits = nks * UPS;
+  SmemLayout L(BITS, SZB, D, a.max_steps, M, WPC, S);
+  unsigned char* ring = smem + L.ring + warp * D * L.stage;
+  uint64_t* bars = (uint64_t*)(smem + L.bars) + warp * D;
+  float* xu = (float*)(smem + L.xu);   // [token][unit] sum of fixed-point x
+  float* su = (float*)(smem + L.su);   // [token][unit] 2^(E-30)
+  float* yp = (float*)(smem + L.yp);
+
+  const char* wsrc = (const char*)(a.qw + ((int64_t)(active ? p : 0) * a.KS) * BITS * 32);
+  const char* zsrc = (const char*)(a.qsz + (int64_t)(active ? p : 0) * a.Gp * 16);
+  auto issue = [&](int s) {  // lane 0: superstep s of the chunk into slot s % D
+    const int slot = s % D;
+    unsigned char* dst = ring + slot * L.stage;
+    mbar_expect_tx(&bars[slot], (uint32_t)L.stage);
+    bulk_g2s(dst, wsrc + (int64_t)(ks0 + s) * BITS * 512, BITS * 512, &bars[slot]);
+    if (SZB) bulk_g2s(dst + BITS * 512, zsrc + (int64_t)(ks0 + s) * SZB, SZB, &bars[slot]);
+  };
+  trace_point(a, 0);
+
+  // ---- 1. ring setup + weight prefetch (independent of the previous kernel) --
+  const int n_first = active ? min(D, nks) : 0;
+  const int n_pre = min(a.pre, n_first);
+  if (lane == 0) {
+    for (int i = 0; i < D; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < n_pre; ++s) issue(s);
+  }
+  if (threadIdx.x < 4) ((uint32_t*)(smem + L.zero))[threadIdx.x] = 0u;
+  __syncwarp();
+
+  // ---- 2. PDL: everything below may read what the previous kernel wrote -----
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  trace_point(a, 1);
+
+  // ---- 3. activation prologue: per-unit exponent, digits, unit sums ---------
   {
-    float mx[2 * NB];
+    const int64_t k0 = (int64_t)ks0 * kSuper;
+    const int items = M * nsteps * 8;  // item = (token, step, half, t): 4 consecutive k
+    uint32_t* bw = (uint32_t*)(smem + L.bfrag);
+    constexpr int RB = 4;  // rounds of item loads kept in flight together
+    const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
+    const int rounds = (items + T - 1) / T;
+    bool first = true;
+    for (int r0 = 0; r0 < rounds; r0 += RB) {  // CTA-uniform trip count
+      float v[RB][4];
 #pragma unroll
-    for (int tk = 0; tk < 2 * NB; ++tk) mx[tk] = 0.f;
-    for (int64_t k = k0 + threadIdx.x; k < kend; k += T)
+      for (int r = 0; r < RB; ++r) {
+        const int it = (r0 + r) * T + threadIdx.x;
+        v[r][0] = v[r][1] = v[r][2] = v[r][3] = 0.f;
+        if (it < items) {
+          const int sub = it & 7, st = (it >> 3) % nsteps, tk = (it >> 3) / nsteps;
+          load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v[r]);
+        }
+      }
+      if (first) {  // the rest of the first ring fill goes out behind the x loads
+        first = false;
+        if (lane == 0)
+          for (int s = n_pre; s < n_first; ++s) issue(s);
+      }
 #pragma unroll
-      for (int tk = 0; tk < 2 * NB; ++tk)
-        if (tk < M) mx[tk] = fmaxf(mx[tk], fabsf(load_x(a.x, a.x_dtype, tk * a.ldx + k)));
+      for (int r = 0; r < RB; ++r) {
+        if (r0 + r >= rounds) break;  // uniform
+        const int it = (r0 + r) * T + threadIdx.x;
+        const bool live = it < items;
+        const int sub = it & 7, st = (it >> 3) % nsteps, tk = live ? (it >> 3) / nsteps : 0;
+        // unit max |x| (REDUX on the order-preserving bit pattern of |x| >= 0)
+        const float m4 = fmaxf(fmaxf(fabsf(v[r][0]), fabsf(v[r][1])), fmaxf(fabsf(v[r][2]), fabsf(v[r][3])));
+        const uint32_t umx = __reduce_max_sync(umask, __float_as_uint(m4));
+        // max < 2^e; e from the biased exponent (denormal max: 2^-126 still bounds it)
+        const int e = umx ? (int)((umx >> 23) & 0xFF) - 126 : 0;
+        const int k = 30 - e, k1 = k >> 1, k2 = k - k1;  // 2^k may leave the f32 range
+        const float f1 = __int_as_float((127 + k1) << 23), f2 = __int_as_float((127 + k2) << 23);
+        int mv[4];
 #pragma unroll
-    for (int tk = 0; tk < 2 * NB; ++tk) {
-      float v = mx[tk];
-      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0) red[tk * 32 + warp] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < 2 * NB) {
-      float v = 0.f;
-      for (int w = 0; w < WPC; ++w) v = fmaxf(v, red[threadIdx.x * 32 + w]);
-      int e = 0;
-      if (v > 0.f) frexpf(v, &e);  // v < 2^e
-      expo[threadIdx.x] = e;
-    }
-    __syncthreads();
-    // items: (token, step, half, t) -> 4 consecutive k; 8 items of a step are
-    // 8 consecutive lanes so their X partial sums reduce with shuffles.
-    const int items = 2 * NB * nsteps * 8;
-    for (int it0 = 0; it0 < items; it0 += T) {
-      const int it = it0 + threadIdx.x;
-      const bool live = it < items;
-      const int sub = it & 7, hh = sub >> 2, tt = sub & 3;
-      const int st = (it >> 3) % nsteps, tk = (it >> 3) / nsteps;
-      const int64_t kb = k0 + 32 * st + 16 * hh + 4 * tt;
-      long long xsum = 0;
-      uint32_t dw[4] = {0u, 0u, 0u, 0u};
-      if (live && tk < M) {
-        const int sh = 30 - expo[tk];
+        for (int i = 0; i < 4; ++i) mv[i] = __float2int_rn(__fmul_rn(__fmul_rn(v[r][i], f1), f2));
+        // balanced base-256 digits: with t = m + 0x808080, digit j < 3 is byte j of t
+        // minus 128 (i.e. byte ^ 0x80 as s8) and the top digit is t >> 24 (|.| <= 64)
+        uint32_t tt[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tt[i] = (uint32_t)(mv[i] + 0x808080);
+        const uint32_t lo01 = __byte_perm(tt[0], tt[1], 0x5140), lo23 = __byte_perm(tt[2], tt[3], 0x5140);
+        const uint32_t hi01 = __byte_perm(tt[0], tt[1], 0x7362), hi23 = __byte_perm(tt[2], tt[3], 0x7362);
+        const uint32_t dw3 = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // byte 0 of each
+        const uint32_t dw2 = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // byte 1
+        const uint32_t dw1 = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // byte 2
+        const uint32_t dw0 = __byte_perm(hi01, hi23, 0x7632);                // byte 3 = t >> 24
+        // exact unit sum of m, split 16/16 so each half fits an int32 REDUX
+        int slo = 0, shi = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int64_t k = kb + i;
-          const float xv = (k < a.n) ? load_x(a.x, a.x_dtype, tk * a.ldx + k) : 0.f;
-          const int mv = __double2int_rn(scalbn((double)xv, sh));
-          xsum += mv;
-          const int d3 = sbyte(mv);
-          const int m1 = (mv - d3) >> 8;
-          const int d2 = sbyte(m1);
-          const int m2 = (m1 - d2) >> 8;
-          const int d1 = sbyte(m2);
-          const int d0 = (m2 - d1) >> 8;
-          dw[0] |= (uint32_t)(d0 & 0xFF) << (8 * i);
-          dw[1] |= (uint32_t)(d1 & 0xFF) << (8 * i);
-          dw[2] |= (uint32_t)(d2 & 0xFF) << (8 * i);
-          dw[3] |= (uint32_t)(d3 & 0xFF) << (8 * i);
+          slo += mv[i] & 0xFFFF;
+          shi += mv[i] >> 16;
+        }
+        slo = __reduce_add_sync(umask, slo);
+        shi = __reduce_add_sync(umask, shi);
+        if (live) {
+          // [step][token][digit j][t] x (b0, b1): read by lane (gq, t), gq % 4 == j
+          uint32_t* dst = bw + ((st * M + tk) * 16 + (sub & 3)) * 2 + (sub >> 2);
+          dst[0] = dw0;
+          dst[8] = dw1;
+          dst[16] = dw2;
+          dst[24] = dw3;
+          if ((it % IPU) == 0) {
+            const int u = tk * nunits + (it % (nsteps * 8)) / IPU;
+            xu[u] = fmaf((float)shi, 65536.f, (float)slo);
+            su[u] = scalbnf(1.f, e - 30);
+          }
         }
       }
-      if (live) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = tk * 4 + j;
-          uint32_t* dst = (uint32_t*)&bfrag[(st * NB + (col >> 3)) * 32 + (col & 7) * 4 + tt];
-          dst[hh] = dw[j];
-        }
-      }
-      for (int o = 1; o < 8; o <<= 1) xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
-      if (live && sub == 0 && tk < M) xstep[st * M + tk] = (double)xsum;
     }
-    __syncthreads();
-    // X over each flush range (group ∩ chunk), in units of 2^(E-30)
-    const int64_t ge = a.g ? a.g : (int64_t)a.KS * kSuper;
-    const int gi0 = (int)(k0 / ge);
-    const int gi1 = (int)(((int64_t)ks1 * kSuper - 1) / ge);
-    const int nr = gi1 - gi0 + 1;
-    for (int e = threadIdx.x; e < nr * M; e += T) {
-      const int r = e / M, tk = e % M;
-      const int64_t lo = max((int64_t)(gi0 + r) * ge, k0), hi = min((int64_t)(gi0 + r + 1) * ge, (int64_t)ks1 * kSuper);
-      double s = 0.0;
-      for (int st = (int)((lo - k0) / 32); st < (int)((hi - k0) / 32); ++st) s += xstep[st * M + tk];
-      xr[r * M + tk] = (float)s;
-    }
+    if (first && lane == 0)  // no activation items (cannot happen for n > 0)
+      for (int s = n_pre; s < n_first; ++s) issue(s);
     __syncthreads();
   }
+  asm volatile("griddepcontrol.launch_dependents;");
+  trace_point(a, 2);
 
-  // ---- 4. main loop ---------------------------------------------------------
-  const int64_t ge = a.g ? a.g : (int64_t)a.KS * kSuper;
-  const int steps_per_group = (int)(ge / kStep);
-  const int gi0 = (int)(k0 / ge);
-  int acc[NB][4];
+  // ---- 4. main loop ------------------------------------------------------------
+  // AC accumulator sets alternate over steps: AC independent IMMA chains
+  constexpr int AC = NB <= 2 ? 2 : 1;
+  int acc[AC][NB][4];
   float yv[NB][2];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
     yv[nb][0] = yv[nb][1] = 0.f;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[nb][q] = 0;
+    for (int c = 0; c < AC; ++c)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[c][nb][q] = 0;
   }
-  const float2* szp = a.qsz + (int64_t)(active ? p : 0) * a.Gp * 16;
-  float2 sz0 = szp[gi0 * 16 + gq], sz1 = szp[gi0 * 16 + gq + 8];
   const float wscale = (t & 1) ? 1.f : 65536.f;
-  int gcur = gi0;
-  const int sg0 = ks0 * 8;  // global step index of the chunk start
-
-  for (int s0 = 0; s0 < nks; s0 += D) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int s = s0 + d;
-      if (s < nks) {
-#pragma unroll
-        for (int sl = 0; sl < 8; ++sl) {
-          uint32_t af[4];
-          extract<BITS>(buf[d], sl, af);
-          const int st = s * 8 + sl;
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb) imma(acc[nb], af, bfrag[(st * NB + nb) * 32 + lane]);
-          const int gstep = sg0 + st + 1;
-          if ((gstep % steps_per_group) == 0 || st + 1 == nsteps) {
-            // flush: y += s * (A - z * X) for range (gcur ∩ chunk)
-            const int r = gcur - gi0;
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb) {
-              const int tk = 2 * nb + (t >> 1);
-              const float X = ((t & 1) == 0 && tk < M) ? xr[r * M + tk] : 0.f;
-              // digit pair (d_2h, d_2h+1) of this lane: value = (acc_hi*256 + acc_lo)*w
-              const float a0 = fmaf((float)acc[nb][0], 256.f * wscale, (float)acc[nb][1] * wscale);
-              const float a1 = fmaf((float)acc[nb][2], 256.f * wscale, (float)acc[nb][3] * wscale);
-              const float f0 = fmaf(-sz0.y, X, a0);
-              const float f1 = fmaf(-sz1.y, X, a1);
-              yv[nb][0] = fmaf(sz0.x, f0, yv[nb][0]);
-              yv[nb][1] = fmaf(sz1.x, f1, yv[nb][1]);
-              acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0;
-            }
-            ++gcur;
-            if (gcur < a.Gp) {
-              sz0 = szp[gcur * 16 + gq];
-              sz1 = szp[gcur * 16 + gq + 8];
-            }
-          }
-        }
-        if (s + D < nks && active) {
-#pragma unroll
-          for (int v = 0; v < BITS; ++v) buf[d][v] = ldg_stream(wp + ((s + D) * BITS + v) * 32);
-        }
-      }
-    }
-  }
-
-  // ---- 5. combine digit-pair lanes, undo the fixed-point scale -------------
+  // B fragment of n8 block nb: token 2nb + (gq >> 2), digit gq & 3 (zeros past M)
+  const uint2* bsrc[NB];
+  int bstride[NB];
+  const float* xul[NB];
+  const float* sul[NB];
+  bool xon[NB];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
-    float v0 = yv[nb][0] + __shfl_xor_sync(0xffffffffu, yv[nb][0], 1);
-    float v1 = yv[nb][1] + __shfl_xor_sync(0xffffffffu, yv[nb][1], 1);
+    const int tb = 2 * nb + (gq >> 2);
+    bsrc[nb] = tb < M ? (const uint2*)(smem + L.bfrag) + tb * 16 + (gq & 3) * 4 + t
+                      : (const uint2*)(smem + L.zero);
+    bstride[nb] = tb < M ? M * 16 : 0;
+    const int tc = 2 * nb + (t >> 1);  // token of this lane's accumulator columns
+    xon[nb] = ((t & 1) == 0) && tc < M;
+    xul[nb] = xu + (tc < M ? tc : 0) * nunits;
+    sul[nb] = su + (tc < M ? tc : 0) * nunits;
+  }
+  const float2* szg = (const float2*)zsrc;
+  const int spg = a.g ? a.g / kStep : a.KS * 8;  // steps per group
+  int gcur = ks0 * 8 / spg;
+  float2 szr0 = make_float2(0.f, 0.f), szr1 = szr0;
+  if (GPS == 0) {
+    szr0 = szg[gcur * 16 + gq];
+    szr1 = szg[gcur * 16 + gq + 8];
+  }
+  auto flush = [&](int u, float2 sz0, float2 sz1) {
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const float X = xon[nb] ? xul[nb][u] : 0.f;
+      const float sc = sul[nb][u];
+      int c0 = acc[0][nb][0], c1 = acc[0][nb][1], c2 = acc[0][nb][2], c3 = acc[0][nb][3];
+#pragma unroll
+      for (int c = 1; c < AC; ++c) {
+        c0 += acc[c][nb][0]; c1 += acc[c][nb][1]; c2 += acc[c][nb][2]; c3 += acc[c][nb][3];
+      }
+      const float a0 = fmaf((float)c0, 256.f * wscale, (float)c1 * wscale);
+      const float a1 = fmaf((float)c2, 256.f * wscale, (float)c3 * wscale);
+      yv[nb][0] = fmaf(sz0.x * sc, fmaf(-sz0.y, X, a0), yv[nb][0]);
+      yv[nb][1] = fmaf(sz1.x * sc, fmaf(-sz1.y, X, a1), yv[nb][1]);
+#pragma unroll
+      for (int c = 0; c < AC; ++c) acc[c][nb][0] = acc[c][nb][1] = acc[c][nb][2] = acc[c][nb][3] = 0;
+    }
+  };
+
+  int slot = 0;
+  uint32_t phase = 0;
+  const int my_nks = active ? nks : 0;  // idle warps never wait on their ring
+  for (int s = 0; s < my_nks; ++s) {
+    mbar_wait(&bars[slot], phase);
+    const unsigned char* stg = ring + slot * L.stage;
+    uint4 w[BITS];
+#pragma unroll
+    for (int v = 0; v < BITS; ++v) w[v] = ((const uint4*)stg)[v * 32 + lane];
+    const float2* szs = (const float2*)(stg + BITS * 512);
+    const int st0 = s * 8;
+#pragma unroll
+    for (int sl = 0; sl < 8; ++sl) {
+      uint32_t af[4];
+      extract<BITS>(w, sl, af);
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) imma(acc[sl % AC][nb], af, bsrc[nb][(st0 + sl) * bstride[nb]]);
+      if ((sl + 1) % SPU == 0) {
+        const int uj = (sl + 1) / SPU - 1;  // unit within the superstep
+        const int u = s * UPS + uj;
+        if (GPS > 0) {
+          const int gi = GPS >= UPS ? uj : 0;  // g = 256: both units use group 0
+          flush(u, szs[gi * 16 + gq], szs[gi * 16 + gq + 8]);
+        } else {
+          flush(u, szr0, szr1);
+        }
+      }
+    }
+    if (GPS == 0 && ((ks0 + s + 1) * 8) % spg == 0) {  // long group closed
+      ++gcur;
+      if (gcur < a.Gp) {
+        szr0 = szg[gcur * 16 + gq];
+        szr1 = szg[gcur * 16 + gq + 8];
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && s + D < nks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(s + D);
+    }
+    if (++slot == D) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+  trace_point(a, 3);
+
+  // ---- 5. combine digit-pair lanes; deterministic split-K reduction ---------
+  // Element e = (warp*16 + row)*M + token of this CTA column; with S > 1 the
+  // S CTAs of the cluster each own a slice of Rs elements and every CTA pushes
+  // its partial into the owner's shared memory (slot = its rank), then one
+  // cluster barrier, then owners sum their slots in rank order.
+  const int R = WPC * 16 * M;
+  const int Rs = (R + S - 1) / S;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = S > 1 ? (int)cluster.block_rank() : 0;
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    const float v0 = yv[nb][0] + __shfl_xor_sync(0xffffffffu, yv[nb][0], 1);
+    const float v1 = yv[nb][1] + __shfl_xor_sync(0xffffffffu, yv[nb][1], 1);
     const int tk = 2 * nb + (t >> 1);
     if ((t & 1) == 0 && tk < M) {
-      const int sh = expo[tk] - 30;
-      yp[(warp * 16 + gq) * M + tk] = scalbnf(v0, sh);
-      yp[(warp * 16 + gq + 8) * M + tk] = scalbnf(v1, sh);
+      const int e0 = (warp * 16 + gq) * M + tk, e1 = (warp * 16 + gq + 8) * M + tk;
+      if (S == 1) {
+        yp[e0] = v0;
+        yp[e1] = v1;
+      } else {
+        cluster.map_shared_rank(yp, e0 / Rs)[rank * Rs + e0 % Rs] = v0;
+        cluster.map_shared_rank(yp, e1 / Rs)[rank * Rs + e1 % Rs] = v1;
+      }
     }
   }
-
-  // ---- 6. deterministic split-K reduction across the cluster ---------------
-  const int R = WPC * 16 * M;
-  const int64_t col0 = (int64_t)blockIdx.x * WPC * 16;
   if (S == 1) {
     __syncthreads();
-    for (int e = threadIdx.x; e < R; e += T) {
-      const int64_t col = col0 + e / M;
-      const int tk = e % M;
-      if (col < a.m) {
-        float* dst = a.y + tk * a.ldy + col;
-        *dst = a.accumulate ? *dst + yp[e] : yp[e];
-      }
-    }
   } else {
-    cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();
-    const int rank = (int)cluster.block_rank();
-    const int e0 = (int)((int64_t)R * rank / S), e1 = (int)((int64_t)R * (rank + 1) / S);
-    for (int e = e0 + threadIdx.x; e < e1; e += T) {
-      float v = 0.f;
-      for (int q = 0; q < S; ++q) v += cluster.map_shared_rank(yp, q)[e];
-      const int64_t col = col0 + e / M;
-      const int tk = e % M;
-      if (col < a.m) {
-        float* dst = a.y + tk * a.ldy + col;
-        *dst = a.accumulate ? *dst + v : v;
-      }
-    }
-    cluster.sync();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
+  const int64_t col0 = (int64_t)blockIdx.x * WPC * 16;
+  const int e_lo = S == 1 ? 0 : rank * Rs;
+  const int e_hi = S == 1 ? R : min(R, e_lo + Rs);
+  for (int e = e_lo + threadIdx.x; e < e_hi; e += T) {
+    float v;
+    if (S == 1) {
+      v = yp[e];
+    } else {
+      v = 0.f;
+      for (int q = 0; q < S; ++q) v += yp[q * Rs + (e - e_lo)];
+    }
+    const int64_t col = col0 + e / M;
+    const int tk = e % M;
+    if (col < a.m) {
+      float* dst = a.y + tk * a.ldy + col;
+      *dst = a.accumulate ? *dst + v : v;
+    }
+  }
+  trace_point(a, 4);
 }
 
 // ---------------------------------------------------------------------------
-constexpr int kWPC = 4;
+static unsigned long long* g_trace = nullptr;
+constexpr int kMaxSplits = 16;  // cluster size along K (non-portable above 8)
+static int g_pre = -1;  // stages issued before the PDL wait (-1: all of the first fill)
 
-template <int BITS, int NB>
-static int launch_nb(const GemvArgs& a, int S, cudaStream_t stream) {
-  constexpr int D = BITS == 2 ? 4 : (BITS == 3 ? 3 : 2);
-  auto kern = gemv_kernel<BITS, NB, kWPC, D>;
-  SmemLayout L(a.max_steps, NB, a.M, a.max_ranges, kWPC);
-  static int configured_bytes = 0;
-  if (L.total > 48 * 1024 && L.total > configured_bytes) {
-    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
-    configured_bytes = L.total;
+static int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+template <int BITS, int NB, int WPC, int GPS>
+static int launch_cfg(GemvArgs& a, int S, cudaStream_t stream) {
+  auto kern = gemv_kernel<BITS, NB, WPC, GPS>;
+  const int max_ks = (a.KS + S - 1) / S;
+  a.max_steps = max_ks * 8;
+  const int stage = BITS * 512 + GPS * 128;
+  // ring: up to ~96 KB of stages per CTA, never more than the chunk
+  SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, a.M, WPC, S);
+  const int budget = std::min(88 * 1024, 224 * 1024 - L0.total - WPC * 16);
+  a.D = std::max(2, std::min(max_ks, budget / (WPC * stage)));
+  a.pre = g_pre < 0 ? a.D : g_pre;
+  SmemLayout L(BITS, GPS * 128, a.D, a.max_steps, a.M, WPC, S);
+  QIGEN_CHECK_ARG(L.total <= 227 * 1024, QIGEN_ERR_UNSUPPORTED,
+                  "GEMV needs %d bytes of shared memory (K chunk too long; raise k_splits)",
+                  L.total);
+  static bool configured = false;
+  if (!configured) {
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024));
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((a.P + kWPC - 1) / kWPC), (unsigned)S, 1);
-  cfg.blockDim = dim3(kWPC * 32, 1, 1);
+  cfg.gridDim = dim3((unsigned)((a.P + WPC - 1) / WPC), (unsigned)S, 1);
+  cfg.blockDim = dim3(WPC * 32, 1, 1);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
@@ -393,40 +560,57 @@ static int launch_nb(const GemvArgs& a, int S, cudaStream_t stream) {
   return QIGEN_OK;
 }
 
-template <int BITS>
-static int launch_bits(const GemvArgs& a, int S, cudaStream_t stream) {
-  const int nb = (a.M + 1) / 2;
-  if (nb <= 1) return launch_nb<BITS, 1>(a, S, stream);
-  if (nb <= 2) return launch_nb<BITS, 2>(a, S, stream);
-  if (nb <= 4) return launch_nb<BITS, 4>(a, S, stream);
-  return launch_nb<BITS, 8>(a, S, stream);
-}
-
-static int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
+template <int BITS, int NB, int WPC>
+static int launch_gps(GemvArgs& a, int S, cudaStream_t stream) {
+  switch (a.g) {
+    case 32: return launch_cfg<BITS, NB, WPC, 8>(a, S, stream);
+    case 64: return launch_cfg<BITS, NB, WPC, 4>(a, S, stream);
+    case 128: return launch_cfg<BITS, NB, WPC, 2>(a, S, stream);
+    case 256: return launch_cfg<BITS, NB, WPC, 1>(a, S, stream);
+    default: return launch_cfg<BITS, NB, WPC, 0>(a, S, stream);
   }
-  return cached;
 }
 
-// K split: enough warps to cover DRAM latency (~16 per SM), at most 8 CTAs
-// per cluster, at least one superstep per chunk.
-int choose_splits(int64_t P, int KS, int M) {
-  const int64_t target = (int64_t)sm_count() * 16;
-  int64_t S = (target + P - 1) / P;
-  S = std::max<int64_t>(1, std::min<int64_t>({S, 8, (int64_t)KS}));
-  (void)M;
-  return (int)S;
+template <int BITS, int WPC>
+static int launch_nb(GemvArgs& a, int S, cudaStream_t stream) {
+  const int nb = (a.M + 1) / 2;
+  if (nb <= 1) return launch_gps<BITS, 1, WPC>(a, S, stream);
+  if (nb <= 2) return launch_gps<BITS, 2, WPC>(a, S, stream);
+  if (nb <= 4) return launch_gps<BITS, 4, WPC>(a, S, stream);
+  return launch_gps<BITS, 8, WPC>(a, S, stream);
+}
+
+// Launch shape: WPC panels (warps) per CTA sharing one K-chunk, S K-chunks per
+// cluster (<= 8, portable).  One wave only: the grid stays within ~90% of the
+// 2-CTA-per-SM capacity (clusters must pack into GPCs); among those, the
+// largest S (shortest chunk).
+static void choose_shape(int P, int KS, int req_S, int& WPC, int& S) {
+  const int sms = sm_count();
+  WPC = 8;  // 2 CTAs (16 warps) per SM
+  const int cols = (P + WPC - 1) / WPC;
+  if (req_S > 0) {
+    S = req_S;
+    return;
+  }
+  const int slots = (2 * sms * 9) / 10;
+  S = 1;
+  for (int c = 2; c <= std::min(8, KS); ++c)
+    if (cols * c <= slots) S = c;
 }
 
 }  // namespace qigen
 
 using namespace qigen;
 
+extern "C" int qigen_debug_trace(void* buf) {
+  g_trace = (unsigned long long*)buf;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_prefetch(int stages_before_wait) {
+  g_pre = stages_before_wait;
+  return QIGEN_OK;
+}
 extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
                           int64_t group, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
                           float* y, int64_t ldy, int accumulate, int k_splits, void* stream) {
@@ -436,13 +620,17 @@ extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64
   QIGEN_CHECK_ARG(n > 0 && m > 0, QIGEN_ERR_ARG, "empty matrix");
   QIGEN_CHECK_ARG(group == 0 || (n % group == 0), QIGEN_ERR_CONFIG,
                   "group size %lld does not divide row count %lld", (long long)group, (long long)n);
-  QIGEN_CHECK_ARG(group == 0 || group % kStep == 0, QIGEN_ERR_UNSUPPORTED,
-                  "group size %lld: the GEMV needs a multiple of 32", (long long)group);
+  QIGEN_CHECK_ARG(group == 0 || group == 32 || group == 64 || group == 128 || group % kSuper == 0,
+                  QIGEN_ERR_UNSUPPORTED,
+                  "group size %lld: the GEMV takes 32, 64, 128 or a multiple of 256 (or full "
+                  "column)", (long long)group);
   QIGEN_CHECK_ARG(tokens >= 1 && tokens <= 16, QIGEN_ERR_UNSUPPORTED,
                   "the GEMV path takes 1..16 activation rows, got %lld", (long long)tokens);
   QIGEN_CHECK_ARG(x_dtype >= 0 && x_dtype <= 2, QIGEN_ERR_ARG, "bad x dtype %d", x_dtype);
   QIGEN_CHECK_ARG(ldx >= n && ldy >= m, QIGEN_ERR_ARG, "leading dimensions too small");
-  GemvArgs a;
+  QIGEN_CHECK_ARG(k_splits >= 0 && k_splits <= kMaxSplits, QIGEN_ERR_ARG,
+                  "k_splits %d out of range", k_splits);
+  GemvArgs a = {};
   a.qw = (const uint4*)qw;
   a.qsz = (const float2*)qsz;
   a.x = x;
@@ -457,17 +645,19 @@ extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64
   a.g = (int)group;
   a.M = (int)tokens;
   a.x_dtype = x_dtype;
+  const int esz = x_dtype == QIGEN_F32 ? 4 : 2;
+  a.x_vec = ((uintptr_t)x % 16 == 0) && ((ldx * esz) % 16 == 0);
   a.accumulate = accumulate;
-  int S = k_splits > 0 ? k_splits : choose_splits(a.P, a.KS, a.M);
-  QIGEN_CHECK_ARG(S >= 1 && S <= 8 && S <= a.KS, QIGEN_ERR_ARG, "k_splits %d out of range", S);
-  const int max_ks = (a.KS + S - 1) / S;
-  a.max_steps = max_ks * 8;
-  const int64_t ge = group ? group : (int64_t)a.KS * kSuper;
-  a.max_ranges = (int)((int64_t)max_ks * kSuper / ge) + 2;
+  a.trace = g_trace;
+  int WPC, S;
+  choose_shape(a.P, a.KS, k_splits, WPC, S);
+  QIGEN_CHECK_ARG(S >= 1 && S <= a.KS, QIGEN_ERR_ARG, "k_splits %d out of range", S);
   cudaStream_t s = (cudaStream_t)stream;
+#define QIGEN_LAUNCH(B) return launch_nb<B, 8>(a, S, s)
   switch (bits) {
-    case 2: return launch_bits<2>(a, S, s);
-    case 3: return launch_bits<3>(a, S, s);
-    default: return launch_bits<4>(a, S, s);
+    case 2: QIGEN_LAUNCH(2);
+    case 3: QIGEN_LAUNCH(3);
+    default: QIGEN_LAUNCH(4);
   }
+#undef QIGEN_LAUNCH
 }

@@ -1,0 +1,51 @@
+"""Steady-state timeline: a CUDA graph of back-to-back GEMVs (PDL), each
+launch tracing its CTAs (globaltimer) into its own buffer."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2307_03738_b200 as q  # noqa: E402
+from paper_2307_03738_b200 import _lib  # noqa: E402
+
+dev = torch.device("cuda")
+L = _lib.lib()
+for shp, b, g in [((4096, 4096), 4, 128), ((4096, 11008), 4, 128), ((11008, 4096), 3, 64)]:
+    K, N = shp
+    cfg = q.QuantConfig(b, g)
+    base = q.PanelWeights.from_float(torch.randn(K, N, device=dev) * 0.02, cfg)
+    R = 16
+    pws = [base] + [q.PanelWeights(base.qw.clone(), base.qsz.clone(), K, N, cfg) for _ in range(R - 1)]
+    xs = [torch.randn(K, device=dev) for _ in range(R)]
+    ys = [torch.empty(N, device=dev) for _ in range(R)]
+    bufs = [torch.zeros(4096 * 8, dtype=torch.int64, device=dev) for _ in range(R)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for pw, x, y in zip(pws, xs, ys):
+            pw.gemv(x, out=y)
+        s.synchronize()
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=s):
+            for i, (pw, x, y) in enumerate(zip(pws, xs, ys)):
+                L.qigen_debug_trace(bufs[i].data_ptr())
+                pw.gemv(x, out=y)
+            L.qigen_debug_trace(None)
+        for _ in range(3):
+            gph.replay()
+        s.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        gph.replay()
+        e1.record(s)
+        s.synchronize()
+    print(f"K={K} N={N} b={b} g={g}: {R} GEMVs in {e0.elapsed_time(e1)*1e3:.1f} us "
+          f"({e0.elapsed_time(e1)*1e3/R:.2f} us each, {base.nbytes_algorithmic()*R/e0.elapsed_time(e1)/1e6:.0f} GB/s)")
+    tr = [b_.view(-1, 8).cpu().numpy() for b_ in bufs]
+    t0 = min(t[t[:, 0] > 0][:, 0].min() for t in tr)
+    for i, t in enumerate(tr[:6]):
+        t = t[t[:, 0] > 0]
+        rel = (t[:, :5] - t0) / 1e3
+        print(f"  #{i} ctas {len(t)} entry {rel[:,0].min():6.2f}-{rel[:,0].max():6.2f}  wait {rel[:,1].min():6.2f}-{rel[:,1].max():6.2f}"
+              f"  prol {np.median(rel[:,2]):6.2f}  loop {np.median(rel[:,3]):6.2f} (max {rel[:,3].max():6.2f})  exit {rel[:,4].min():6.2f}-{rel[:,4].max():6.2f}")
