@@ -103,6 +103,9 @@ __device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint2 
 }
 
 // Fragment registers of local step sl (0..7) from the lane's superstep words.
+// Codes stay in place (one AND each); every accumulator row then carries a
+// power-of-two scale: RowScale<BITS>::hi for rows gq+8 (rows gq: 1), and for
+// 2-bit odd steps a further x16 on both rows (kept in the odd accumulator set).
 template <int BITS>
 __device__ __forceinline__ void extract(const uint4 (&w)[BITS], int sl, uint32_t (&a)[4]);
 
@@ -110,21 +113,23 @@ template <>
 __device__ __forceinline__ void extract<4>(const uint4 (&w)[4], int sl, uint32_t (&a)[4]) {
   const uint4 u = w[sl >> 1];
   const uint32_t A = (sl & 1) ? u.z : u.x, B = (sl & 1) ? u.w : u.y;
-  a[0] = A & 0x0F0F0F0Fu;
-  a[1] = (A >> 4) & 0x0F0F0F0Fu;
-  a[2] = B & 0x0F0F0F0Fu;
-  a[3] = (B >> 4) & 0x0F0F0F0Fu;
+  a[0] = A & 0x0F0F0F0Fu;  // rows gq,   k 4t..      x1
+  a[1] = A & 0xF0F0F0F0u;  // rows gq+8, k 4t..      x16
+  a[2] = B & 0x0F0F0F0Fu;  // rows gq,   k 16+4t..   x1
+  a[3] = B & 0xF0F0F0F0u;  // rows gq+8, k 16+4t..   x16
 }
 
 template <>
 __device__ __forceinline__ void extract<2>(const uint4 (&w)[2], int sl, uint32_t (&a)[4]) {
   const uint4 u = w[sl >> 2];
-  const int q = sl & 3;
-  const uint32_t W = q == 0 ? u.x : q == 1 ? u.y : q == 2 ? u.z : u.w;
-  a[0] = W & 0x03030303u;
-  a[1] = (W >> 2) & 0x03030303u;
-  a[2] = (W >> 4) & 0x03030303u;
-  a[3] = (W >> 6) & 0x03030303u;
+  const int q = sl & 2;  // word pair of this step pair
+  const uint32_t X = q == 0 ? u.x : u.z, Y = q == 0 ? u.y : u.w;
+  const uint32_t m0 = (sl & 1) ? 0x30303030u : 0x03030303u;  // x1  (odd: x16)
+  const uint32_t m1 = (sl & 1) ? 0xC0C0C0C0u : 0x0C0C0C0Cu;  // x4  (odd: x64)
+  a[0] = X & m0;
+  a[1] = X & m1;
+  a[2] = Y & m0;
+  a[3] = Y & m1;
 }
 
 __device__ __forceinline__ uint32_t word_of(const uint4 (&w)[3], int q) {
@@ -138,17 +143,22 @@ __device__ __forceinline__ void extract<3>(const uint4 (&w)[3], int sl, uint32_t
   const int pi = sl >> 1;
   const uint32_t A = word_of(w, 3 * pi), B = word_of(w, 3 * pi + 1), C = word_of(w, 3 * pi + 2);
   if ((sl & 1) == 0) {
-    a[0] = A & 0x07070707u;
-    a[1] = (A >> 3) & 0x07070707u;
+    a[0] = A & 0x07070707u;  // x1
+    a[1] = A & 0x38383838u;  // x8
     a[2] = B & 0x07070707u;
-    a[3] = (B >> 3) & 0x07070707u;
+    a[3] = B & 0x38383838u;
   } else {
     a[0] = C & 0x07070707u;
-    a[1] = (C >> 3) & 0x07070707u;
-    a[2] = ((A >> 6) & 0x03030303u) | ((C >> 4) & 0x04040404u);
-    a[3] = ((B >> 6) & 0x03030303u) | ((C >> 5) & 0x04040404u);
+    a[1] = C & 0x38383838u;
+    a[2] = ((A >> 6) & 0x03030303u) | ((C >> 4) & 0x04040404u);  // x1
+    a[3] = ((B >> 3) & 0x18181818u) | ((C >> 2) & 0x20202020u);  // x8
   }
 }
+
+template <int BITS>
+struct RowScale {  // scale of the rows gq+8 accumulators relative to rows gq
+  static constexpr float inv_hi = BITS == 4 ? 1.f / 16.f : BITS == 3 ? 1.f / 8.f : 1.f / 4.f;
+};
 
 __device__ __forceinline__ int sbyte(int v) { return (int)(int8_t)(v & 0xFF); }
 
@@ -193,7 +203,7 @@ struct SmemLayout {
     int off = 0;
     ring = off;  off += WPC * D * stage;
     bars = off;  off += WPC * D * 8;
-    bfrag = off; off += max_steps * M * 128;
+    bfrag = off; off += max_steps * M * 128;  // [token][step][digit j][t] (b0, b1)
     xu = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
     su = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
     zero = off;  off += 16;
@@ -321,8 +331,8 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
         slo = __reduce_add_sync(umask, slo);
         shi = __reduce_add_sync(umask, shi);
         if (live) {
-          // [step][token][digit j][t] x (b0, b1): read by lane (gq, t), gq % 4 == j
-          uint32_t* dst = bw + ((st * M + tk) * 16 + (sub & 3)) * 2 + (sub >> 2);
+          // [token][step][digit j][t] x (b0, b1): read by lane (gq, t), gq % 4 == j
+          uint32_t* dst = bw + ((tk * a.max_steps + st) * 16 + (sub & 3)) * 2 + (sub >> 2);
           dst[0] = dw0;
           dst[8] = dw1;
           dst[16] = dw2;
@@ -343,8 +353,9 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   trace_point(a, 2);
 
   // ---- 4. main loop ------------------------------------------------------------
-  // AC accumulator sets alternate over steps: AC independent IMMA chains
-  constexpr int AC = NB <= 2 ? 2 : 1;
+  // AC accumulator sets alternate over steps: AC independent IMMA chains (2-bit
+  // always uses two: odd steps carry an extra x16)
+  constexpr int AC = (NB <= 2 || BITS == 2) ? 2 : 1;
   int acc[AC][NB][4];
   float yv[NB][2];
 #pragma unroll
@@ -355,19 +366,19 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[c][nb][q] = 0;
   }
-  const float wscale = (t & 1) ? 1.f : 65536.f;
+  // digit-pair weight of this lane: columns (d0, d1) -> 2^16, (d2, d3) -> 1
+  const float w_lo = (t & 1) ? 1.f : 65536.f;
+  const float w_hi = w_lo * RowScale<BITS>::inv_hi;
   // B fragment of n8 block nb: token 2nb + (gq >> 2), digit gq & 3 (zeros past M)
   const uint2* bsrc[NB];
-  int bstride[NB];
   const float* xul[NB];
   const float* sul[NB];
   bool xon[NB];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
     const int tb = 2 * nb + (gq >> 2);
-    bsrc[nb] = tb < M ? (const uint2*)(smem + L.bfrag) + tb * 16 + (gq & 3) * 4 + t
-                      : (const uint2*)(smem + L.zero);
-    bstride[nb] = tb < M ? M * 16 : 0;
+    bsrc[nb] = tb < M ? (const uint2*)(smem + L.bfrag) + tb * a.max_steps * 16 + (gq & 3) * 4 + t
+                      : nullptr;
     const int tc = 2 * nb + (t >> 1);  // token of this lane's accumulator columns
     xon[nb] = ((t & 1) == 0) && tc < M;
     xul[nb] = xu + (tc < M ? tc : 0) * nunits;
@@ -389,12 +400,15 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
       int c0 = acc[0][nb][0], c1 = acc[0][nb][1], c2 = acc[0][nb][2], c3 = acc[0][nb][3];
 #pragma unroll
       for (int c = 1; c < AC; ++c) {
-        c0 += acc[c][nb][0]; c1 += acc[c][nb][1]; c2 += acc[c][nb][2]; c3 += acc[c][nb][3];
+        // 2-bit odd steps: both rows carry an extra exact x16
+        const int sh = BITS == 2 ? 4 : 0;
+        c0 += acc[c][nb][0] >> sh; c1 += acc[c][nb][1] >> sh;
+        c2 += acc[c][nb][2] >> sh; c3 += acc[c][nb][3] >> sh;
       }
-      const float a0 = fmaf((float)c0, 256.f * wscale, (float)c1 * wscale);
-      const float a1 = fmaf((float)c2, 256.f * wscale, (float)c3 * wscale);
-      yv[nb][0] = fmaf(sz0.x * sc, fmaf(-sz0.y, X, a0), yv[nb][0]);
-      yv[nb][1] = fmaf(sz1.x * sc, fmaf(-sz1.y, X, a1), yv[nb][1]);
+      // digit pair -> one exact int32 (|.| < 2^31 for units <= 128 rows)
+      const float q0 = (float)(c0 * 256 + c1), q1 = (float)(c2 * 256 + c3);
+      yv[nb][0] = fmaf(sz0.x * sc, fmaf(-sz0.y, X, q0 * w_lo), yv[nb][0]);
+      yv[nb][1] = fmaf(sz1.x * sc, fmaf(-sz1.y, X, q1 * w_hi), yv[nb][1]);
 #pragma unroll
       for (int c = 0; c < AC; ++c) acc[c][nb][0] = acc[c][nb][1] = acc[c][nb][2] = acc[c][nb][3] = 0;
     }
@@ -416,7 +430,8 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
       uint32_t af[4];
       extract<BITS>(w, sl, af);
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) imma(acc[sl % AC][nb], af, bsrc[nb][(st0 + sl) * bstride[nb]]);
+      for (int nb = 0; nb < NB; ++nb)
+        imma(acc[sl % AC][nb], af, bsrc[nb] ? bsrc[nb][(st0 + sl) * 16] : make_uint2(0u, 0u));
       if ((sl + 1) % SPU == 0) {
         const int uj = (sl + 1) / SPU - 1;  // unit within the superstep
         const int u = s * UPS + uj;

@@ -156,15 +156,20 @@ __global__ void permute_zcurve_kernel(const uint32_t* __restrict__ src, uint32_t
 // the lane owns 4*bits words; element (local step sl in 0..7, fragment
 // register j in 0..3, byte i in 0..3) is
 //     column = 16p + gq + 8*(j & 1),  k = 256s + 32*sl + 16*(j >> 1) + 4t + i
-// i.e. exactly the u8 A-fragment of mma.m16n8k32 for step sl.  How the code
-// bits sit inside the words is chosen so that the GEMV rebuilds each fragment
-// register with one or two shift/LOP3 ops (gemv.cu: extract_*).
+// i.e. exactly the u8 A-fragment of mma.m16n8k32 for step sl.  The bit
+// positions are chosen so that the GEMV rebuilds fragment registers with a
+// single AND mask each (codes left in place, scaled by a power of two that is
+// uniform per accumulator row and undone at the flush; gemv.cu: extract<>):
+//   4-bit: word pair per step; low nibbles = rows gq, high nibbles = rows gq+8.
+//   2-bit: word pair per step pair; 2-bit field 2*(sl&1) + (j&1) of byte i.
+//   3-bit: word triple (A, B, C) per step pair; fields 0-2 / 3-5 of each byte,
+//          the two last registers of the odd step spread over bits 6-7.
 __device__ __forceinline__ void place_code(int bits, uint32_t* wv, int sl, int j, int i,
                                            uint32_t c) {
   if (bits == 4) {
     wv[2 * sl + (j >> 1)] |= c << (8 * i + 4 * (j & 1));
-  } else if (bits == 2) {
-    wv[sl] |= c << (8 * i + 2 * j);
+  } else if (bits == 2) {  // step pair -> words (X, Y); X: a0,a1  Y: a2,a3; odd step in fields 2,3
+    wv[2 * (sl >> 1) + (j >> 1)] |= c << (8 * i + 2 * (2 * (sl & 1) + (j & 1)));
   } else {  // 3-bit: step pair -> words (A, B, C), fragment regs R0..R7
     const int q = 3 * (sl >> 1), R = 4 * (sl & 1) + j;
     if (R < 6) {
@@ -178,7 +183,7 @@ __device__ __forceinline__ void place_code(int bits, uint32_t* wv, int sl, int j
 
 __device__ __forceinline__ uint32_t read_code(int bits, const uint32_t* wv, int sl, int j, int i) {
   if (bits == 4) return (wv[2 * sl + (j >> 1)] >> (8 * i + 4 * (j & 1))) & 15u;
-  if (bits == 2) return (wv[sl] >> (8 * i + 2 * j)) & 3u;
+  if (bits == 2) return (wv[2 * (sl >> 1) + (j >> 1)] >> (8 * i + 2 * (2 * (sl & 1) + (j & 1)))) & 3u;
   const int q = 3 * (sl >> 1), R = 4 * (sl & 1) + j;
   if (R < 6) return (wv[q + (R >> 1)] >> (8 * i + 3 * (R & 1))) & 7u;
   return ((wv[q + (R - 6)] >> (8 * i + 6)) & 3u) | (((wv[q + 2] >> (8 * i + 6 + (R - 6))) & 1u) << 2);
