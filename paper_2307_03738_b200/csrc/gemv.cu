@@ -94,6 +94,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Cluster address of the same shared-memory offset in CTA `rank`.
+__device__ __forceinline__ uint32_t mapa(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+// 4-byte store into another CTA's shared memory, completing tx on its mbarrier.
+__device__ __forceinline__ void st_async(uint32_t addr, float v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   addr),
+               "r"(__float_as_uint(v)), "r"(bar)
+               : "memory");
+}
+
 __device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint2 b) {
   asm volatile(
       "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -196,7 +210,7 @@ __device__ __forceinline__ void load_x4(const GemvArgs& a, int tk, int64_t k, fl
 
 // Shared-memory carve-up (bytes), identical on host and device.
 struct SmemLayout {
-  int ring, bars, bfrag, xu, su, zero, yp, total, stage;
+  int ring, bars, bfrag, xu, su, zero, rbar, yp, total, stage;
   __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int M, int WPC, int S) {
     stage = bits * 512 + szb;
     const int max_units = max_steps;  // units are >= 32 rows
@@ -206,8 +220,9 @@ struct SmemLayout {
     bfrag = off; off += max_steps * M * 128;  // [token][step][digit j][t] (b0, b1)
     xu = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
     su = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
-    zero = off;  off += 16;
-    yp = off;    off += ((WPC * 16 * M + S - 1) / S) * S * 4 + 16;
+    zero = off;  off += 8;
+    rbar = off;  off += 8;
+    yp = off;    off += (S - 1) * WPC * 16 * M * 4 + 16;  // owner's inbox
     total = off;
   }
 };
@@ -219,7 +234,7 @@ struct SmemLayout {
 // fixed-point exponent (found with warp shuffles, no CTA barrier), and the
 // integer accumulators are folded into f32 once per unit.
 template <int BITS, int NB, int WPC, int GPS>
-__global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int T = WPC * 32;
   constexpr int SZB = GPS * 128;
@@ -262,7 +277,27 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < n_pre; ++s) issue(s);
   }
-  if (threadIdx.x < 4) ((uint32_t*)(smem + L.zero))[threadIdx.x] = 0u;
+  if (threadIdx.x < 2) ((uint32_t*)(smem + L.zero))[threadIdx.x] = 0u;
+  uint64_t* rbar = (uint64_t*)(smem + L.rbar);
+  if (S > 1 && threadIdx.x == 0) {
+    // split-K inbox of the cluster's rank-0 CTA: (S-1) partials of R floats
+    mbar_init(rbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(rbar, (uint32_t)((S - 1) * WPC * 16 * M * 4));
+  }
+  if (S > 1)  // arrive now, wait only before pushing: every inbox is initialised by then
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // pull this chunk's activations into L2 now (safe before the PDL wait: L2 is
+  // the point of coherence, and nothing is read into registers or L1 here)
+  {
+    const int esz = a.x_dtype == QIGEN_F32 ? 4 : 2;
+    const int64_t kb = (int64_t)ks0 * kSuper * esz, ke = min((int64_t)ks1 * kSuper, a.n) * esz;
+    const int lines = (int)((ke - kb + 127) / 128);
+    for (int i = threadIdx.x; i < lines * M; i += T) {
+      const char* pa = (const char*)a.x + (i / lines) * a.ldx * esz + kb + (int64_t)(i % lines) * 128;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+    }
+  }
   __syncwarp();
 
   // ---- 2. PDL: everything below may read what the previous kernel wrote -----
@@ -419,6 +454,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   const int my_nks = active ? nks : 0;  // idle warps never wait on their ring
   for (int s = 0; s < my_nks; ++s) {
     mbar_wait(&bars[slot], phase);
+    if (s == 0) trace_point(a, 5);
     const unsigned char* stg = ring + slot * L.stage;
     uint4 w[BITS];
 #pragma unroll
@@ -463,52 +499,39 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   trace_point(a, 3);
 
   // ---- 5. combine digit-pair lanes; deterministic split-K reduction ---------
-  // Element e = (warp*16 + row)*M + token of this CTA column; with S > 1 the
-  // S CTAs of the cluster each own a slice of Rs elements and every CTA pushes
-  // its partial into the owner's shared memory (slot = its rank), then one
-  // cluster barrier, then owners sum their slots in rank order.
+  // Element e = (warp*16 + row)*M + token of this CTA column.  With S > 1 the
+  // CTAs of ranks 1..S-1 push their partials into the rank-0 CTA's inbox with
+  // st.async (completing bytes on its mbarrier) and exit; rank 0 adds them to
+  // its own in rank order (deterministic) and writes y.
   const int R = WPC * 16 * M;
-  const int Rs = (R + S - 1) / S;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = S > 1 ? (int)cluster.block_rank() : 0;
+  const int rank = S > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  if (S > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  trace_point(a, 6);
+  const int64_t col0 = (int64_t)blockIdx.x * WPC * 16;
+  if (rank == 0 && S > 1) mbar_wait(rbar, 0);
+  trace_point(a, 7);
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
     const float v0 = yv[nb][0] + __shfl_xor_sync(0xffffffffu, yv[nb][0], 1);
     const float v1 = yv[nb][1] + __shfl_xor_sync(0xffffffffu, yv[nb][1], 1);
     const int tk = 2 * nb + (t >> 1);
     if ((t & 1) == 0 && tk < M) {
-      const int e0 = (warp * 16 + gq) * M + tk, e1 = (warp * 16 + gq + 8) * M + tk;
-      if (S == 1) {
-        yp[e0] = v0;
-        yp[e1] = v1;
-      } else {
-        cluster.map_shared_rank(yp, e0 / Rs)[rank * Rs + e0 % Rs] = v0;
-        cluster.map_shared_rank(yp, e1 / Rs)[rank * Rs + e1 % Rs] = v1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = warp * 16 + gq + 8 * h;
+        const int e = row * M + tk;
+        float v = h ? v1 : v0;
+        if (rank > 0) {
+          st_async(mapa(yp + (rank - 1) * R + e, 0), v, mapa(rbar, 0));
+        } else {
+          for (int q = 1; q < S; ++q) v += yp[(q - 1) * R + e];
+          const int64_t col = col0 + row;
+          if (col < a.m) {
+            float* dst = a.y + tk * a.ldy + col;
+            *dst = a.accumulate ? *dst + v : v;
+          }
+        }
       }
-    }
-  }
-  if (S == 1) {
-    __syncthreads();
-  } else {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n"
-                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
-  }
-  const int64_t col0 = (int64_t)blockIdx.x * WPC * 16;
-  const int e_lo = S == 1 ? 0 : rank * Rs;
-  const int e_hi = S == 1 ? R : min(R, e_lo + Rs);
-  for (int e = e_lo + threadIdx.x; e < e_hi; e += T) {
-    float v;
-    if (S == 1) {
-      v = yp[e];
-    } else {
-      v = 0.f;
-      for (int q = 0; q < S; ++q) v += yp[q * Rs + (e - e_lo)];
-    }
-    const int64_t col = col0 + e / M;
-    const int tk = e % M;
-    if (col < a.m) {
-      float* dst = a.y + tk * a.ldy + col;
-      *dst = a.accumulate ? *dst + v : v;
     }
   }
   trace_point(a, 4);
@@ -531,20 +554,8 @@ static int sm_count() {
 }
 
 template <int BITS, int NB, int WPC, int GPS>
-static int launch_cfg(GemvArgs& a, int S, cudaStream_t stream) {
+static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   auto kern = gemv_kernel<BITS, NB, WPC, GPS>;
-  const int max_ks = (a.KS + S - 1) / S;
-  a.max_steps = max_ks * 8;
-  const int stage = BITS * 512 + GPS * 128;
-  // ring: up to ~96 KB of stages per CTA, never more than the chunk
-  SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, a.M, WPC, S);
-  const int budget = std::min(88 * 1024, 224 * 1024 - L0.total - WPC * 16);
-  a.D = std::max(2, std::min(max_ks, budget / (WPC * stage)));
-  a.pre = g_pre < 0 ? a.D : g_pre;
-  SmemLayout L(BITS, GPS * 128, a.D, a.max_steps, a.M, WPC, S);
-  QIGEN_CHECK_ARG(L.total <= 227 * 1024, QIGEN_ERR_UNSUPPORTED,
-                  "GEMV needs %d bytes of shared memory (K chunk too long; raise k_splits)",
-                  L.total);
   static bool configured = false;
   if (!configured) {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -552,8 +563,42 @@ static int launch_cfg(GemvArgs& a, int S, cudaStream_t stream) {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
+  const int stage = BITS * 512 + GPS * 128;
+  auto shape = [&](int S) {  // smem plan for S chunks: ring of <= 40 KB per CTA
+    const int max_ks = (a.KS + S - 1) / S;
+    a.max_steps = max_ks * 8;
+    SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, a.M, WPC, S);
+    const int budget = std::min(WPC * 10 * 1024, 224 * 1024 - L0.total - WPC * 16);
+    a.D = std::max(2, std::min(max_ks, budget / (WPC * stage)));
+    return SmemLayout(BITS, GPS * 128, a.D, a.max_steps, a.M, WPC, S);
+  };
+  const int cols = (a.P + WPC - 1) / WPC;
+  int S = req_S;
+  if (S <= 0) {
+    // Empirical rule (tools/tune_splits.py, dependent chains of launches under
+    // PDL on B200): grids above ~1.55 CTAs per SM lose more to the next kernel
+    // not fitting beside this one than they gain from shorter chunks; below
+    // that, the shortest longest-chunk wins (ties: fewer CTAs).
+    const int max_ctas = (sm_count() * 155) / 100;
+    S = 1;
+    int best = a.KS;
+    for (int c = 2; c <= std::min(kMaxSplits, a.KS); ++c) {
+      if (cols * c > max_ctas) break;
+      const int chunk = (a.KS + c - 1) / c;
+      if (chunk < best) {
+        best = chunk;
+        S = c;
+      }
+    }
+  }
+  QIGEN_CHECK_ARG(S >= 1 && S <= a.KS && S <= kMaxSplits, QIGEN_ERR_ARG, "k_splits %d out of range", S);
+  const SmemLayout L = shape(S);
+  a.pre = g_pre < 0 ? a.D : g_pre;
+  QIGEN_CHECK_ARG(L.total <= 227 * 1024, QIGEN_ERR_UNSUPPORTED,
+                  "GEMV needs %d bytes of shared memory (K chunk too long; raise k_splits)",
+                  L.total);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((a.P + WPC - 1) / WPC), (unsigned)S, 1);
+  cfg.gridDim = dim3((unsigned)cols, (unsigned)S, 1);
   cfg.blockDim = dim3(WPC * 32, 1, 1);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = stream;
@@ -593,24 +638,6 @@ static int launch_nb(GemvArgs& a, int S, cudaStream_t stream) {
   if (nb <= 2) return launch_gps<BITS, 2, WPC>(a, S, stream);
   if (nb <= 4) return launch_gps<BITS, 4, WPC>(a, S, stream);
   return launch_gps<BITS, 8, WPC>(a, S, stream);
-}
-
-// Launch shape: WPC panels (warps) per CTA sharing one K-chunk, S K-chunks per
-// cluster (<= 8, portable).  One wave only: the grid stays within ~90% of the
-// 2-CTA-per-SM capacity (clusters must pack into GPCs); among those, the
-// largest S (shortest chunk).
-static void choose_shape(int P, int KS, int req_S, int& WPC, int& S) {
-  const int sms = sm_count();
-  WPC = 8;  // 2 CTAs (16 warps) per SM
-  const int cols = (P + WPC - 1) / WPC;
-  if (req_S > 0) {
-    S = req_S;
-    return;
-  }
-  const int slots = (2 * sms * 9) / 10;
-  S = 1;
-  for (int c = 2; c <= std::min(8, KS); ++c)
-    if (cols * c <= slots) S = c;
 }
 
 }  // namespace qigen
@@ -664,9 +691,7 @@ extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64
   a.x_vec = ((uintptr_t)x % 16 == 0) && ((ldx * esz) % 16 == 0);
   a.accumulate = accumulate;
   a.trace = g_trace;
-  int WPC, S;
-  choose_shape(a.P, a.KS, k_splits, WPC, S);
-  QIGEN_CHECK_ARG(S >= 1 && S <= a.KS, QIGEN_ERR_ARG, "k_splits %d out of range", S);
+  const int S = k_splits;  // 0: chosen per launch shape in launch_cfg
   cudaStream_t s = (cudaStream_t)stream;
 #define QIGEN_LAUNCH(B) return launch_nb<B, 8>(a, S, s)
   switch (bits) {

@@ -46,6 +46,6 @@ for shp, b, g in [((4096, 4096), 4, 128), ((4096, 11008), 4, 128), ((11008, 4096
     t0 = min(t[t[:, 0] > 0][:, 0].min() for t in tr)
     for i, t in enumerate(tr[:6]):
         t = t[t[:, 0] > 0]
-        rel = (t[:, :5] - t0) / 1e3
+        rel = (t[:, :8] - t0) / 1e3
         print(f"  #{i} ctas {len(t)} entry {rel[:,0].min():6.2f}-{rel[:,0].max():6.2f}  wait {rel[:,1].min():6.2f}-{rel[:,1].max():6.2f}"
-              f"  prol {np.median(rel[:,2]):6.2f}  loop {np.median(rel[:,3]):6.2f} (max {rel[:,3].max():6.2f})  exit {rel[:,4].min():6.2f}-{rel[:,4].max():6.2f}")
+              f"  prol {np.median(rel[:,2]):6.2f} stage0 {np.median(rel[:,5]):6.2f} loop {np.median(rel[:,3]):6.2f} (max {rel[:,3].max():6.2f}) push {np.median(rel[:,6]):6.2f} bar {np.median(rel[:,7]):6.2f} exit {rel[:,4].min():6.2f}-{rel[:,4].max():6.2f}")
