@@ -329,6 +329,109 @@ def run_ours(args):
     return 0
 
 
+def run_decode(args):
+    """BASELINE configs[3]/[4]: one decode step of a random-init LLaMA shard per
+    GPU (tensor parallel over the ranks), replayed as a CUDA graph."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2307_03738_b200 import decode as D
+
+    cfg = D.LLAMA_7B if args.workload == "llama7b" else D.LLAMA_65B
+    if args.layers:
+        cfg = D.shrink(cfg, n_layers=args.layers)
+    ctx = args.ctx or (512 if args.workload == "llama7b" else 1024)
+    B = args.batch
+    t0 = time.perf_counter()
+    model = D.LlamaTP(cfg, batch=B, max_ctx=ctx + 1, seed=0, tp=D.TP())
+    setup_s = time.perf_counter() - t0
+    tok = torch.zeros(B, dtype=torch.long, device="cuda")
+    pos = ctx  # ctx past tokens in the cache, this step writes position ctx
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            model.step(tok, pos)
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            nxt = model.step(tok, pos)
+        sampler = ClockSampler(local)
+        with sampler:
+            for _ in range(args.warmup):
+                graph.replay()
+            stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            e1.record(stream)
+            e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    # e2e: token ids in from pinned host memory, next ids back, every step
+    tok_h = torch.zeros(B, dtype=torch.long).pin_memory()
+    out_h = torch.zeros(B, dtype=torch.long).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n_e2e = min(args.steps, 50)
+    w0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        for _ in range(n_e2e):
+            tok.copy_(tok_h, non_blocking=True)
+            graph.replay()
+            out_h.copy_(nxt, non_blocking=True)
+            stream.synchronize()
+    e2e_s = (time.perf_counter() - w0) / n_e2e
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    nbytes = model.bytes_per_step(pos)
+    if world > 1:
+        t = torch.tensor([float(nbytes)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        nbytes = int(t.item())
+    if rank == 0:
+        peak, peak_src = measured_peak()
+        gbs = nbytes / (ms_step / 1e3) / 1e9
+        line = {
+            "metric": "decode tokens/s", "value": round(B / (ms_step / 1e3), 2), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8 x s8 -> s32 (IMMA) linears, f16 KV/lm_head",
+            "data": "synthetic (random-init weights, random fp16 KV cache)",
+            "config": {"workload": f"{args.workload} decode step", "layers": cfg.n_layers,
+                       "d_model": cfg.d_model, "bits": cfg.bits, "group": cfg.group,
+                       "batch": B, "ctx": ctx, "parallelism": f"tp{world}",
+                       "setup_s": round(setup_s, 1)},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": round(gbs / peak, 4),
+                         "bytes_per_step_per_gpu": nbytes, "traffic": None},
+            "e2e": {"value": round(B / e2e_s, 2), "unit": "tokens/s", "h2d_bytes_per_step": 8 * B,
+                    "d2h_bytes_per_step": 8 * B},
+            "gpu_launches": None,
+            "clocks": sampler.report(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def _traffic():
     """DRAM bytes per step from the committed ncu summary, if one exists."""
     p = ROOT / "profiles" / "traffic.json"
@@ -347,11 +450,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["sweep", "llama7b", "llama65b"], default="sweep")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--ctx", type=int, default=0)
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count (smoke runs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload != "sweep":
+        return run_decode(args)
     return run_ours(args)
 
 

@@ -592,6 +592,8 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     }
   }
   QIGEN_CHECK_ARG(S >= 1 && S <= a.KS && S <= kMaxSplits, QIGEN_ERR_ARG, "k_splits %d out of range", S);
+  // many tokens x long chunks: split K further until the fragments fit in smem
+  while (req_S <= 0 && shape(S).total > 200 * 1024 && S < std::min(kMaxSplits, a.KS)) ++S;
   const SmemLayout L = shape(S);
   a.pre = g_pre < 0 ? a.D : g_pre;
   QIGEN_CHECK_ARG(L.total <= 227 * 1024, QIGEN_ERR_UNSUPPORTED,

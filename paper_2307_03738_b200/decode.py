@@ -1,0 +1,296 @@
+"""Tensor-parallel LLaMA-architecture decode driver over the quantized GEMV.
+
+BASELINE configs[3] / [4] (north_star (d)): random-init LLaMA-7B (4-bit, g=128)
+and LLaMA-65B (3-bit, g=64) decode steps, batch 1 (and 8 for 65B), fp16 KV
+cache of 512 / 1024 past tokens, tensor-parallel over the GPUs of one node.
+The reference has no model path; this driver is the consumer the
+quantized GEMV exists for.
+
+Sharding (Megatron pairing, one process per GPU, NCCL):
+  * column-parallel, no communication: fused QKV (heads split across ranks) and
+    fused gate|up (FFN columns split);
+  * row-parallel: o_proj and down_proj take K-shards aligned to whole
+    quantization groups and whole 256-row supersteps (uneven when the group
+    count does not divide, e.g. 7B down_proj K = 11008 = 43 supersteps); rank 0
+    accumulates the residual into its partial inside the GEMV epilogue, then
+    one NCCL all-reduce per row-parallel layer (2 per layer);
+  * lm_head is vocab-parallel (fp16), followed by an all-gather of logits.
+
+Everything runs inside one CUDA graph per decode step.  The quantized linears
+are ``PanelWeights`` (GPU quantize, bit-exact with quant.py, then the IMMA
+GEMV).  A linear *backend* object builds them; tests inject a dequantized CPU
+backend to check the TP logic with gloo (tests/test_decode_tp.py).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import torch
+import torch.nn.functional as F
+
+from .config import QuantConfig
+from .runtime import PanelWeights
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    n_layers: int
+    d_model: int
+    n_heads: int
+    head_dim: int
+    ffn: int
+    vocab: int
+    bits: int
+    group: int | None
+    norm_eps: float = 1e-5
+    rope_theta: float = 10000.0
+
+    @property
+    def qcfg(self) -> QuantConfig:
+        return QuantConfig(self.bits, self.group)
+
+
+LLAMA_7B = LlamaConfig(32, 4096, 32, 128, 11008, 32000, 4, 128)
+LLAMA_65B = LlamaConfig(80, 8192, 64, 128, 22016, 32000, 3, 64)
+
+
+# ---------------------------------------------------------------------------
+# shard arithmetic (pure; tested on CPU)
+# ---------------------------------------------------------------------------
+
+def even_split(total_units: int, world: int, rank: int) -> tuple[int, int]:
+    """Units [lo, hi) of `rank` when `total_units` are spread as evenly as
+    possible (the first `total_units % world` ranks get one more)."""
+    base, extra = divmod(total_units, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def row_shard(K: int, group: int | None, world: int, rank: int) -> tuple[int, int]:
+    """K-range of a row-parallel shard: whole groups and, when they fit, whole
+    256-row supersteps of the GPU panel layout (uneven shards)."""
+    if world == 1:
+        return 0, K
+    if group is None:
+        raise ValueError("row-parallel sharding needs grouped quantization")
+    unit = math.lcm(group, 256) if K % math.lcm(group, 256) == 0 else group
+    if K % unit:
+        raise ValueError(f"K={K} is not a multiple of the group size {group}")
+    lo, hi = even_split(K // unit, world, rank)
+    return lo * unit, hi * unit
+
+
+def head_shard(n_heads: int, world: int, rank: int) -> tuple[int, int]:
+    if n_heads % world:
+        raise ValueError(f"{n_heads} heads do not split over {world} ranks")
+    per = n_heads // world
+    return rank * per, (rank + 1) * per
+
+
+def col_shard(N: int, world: int, rank: int, align: int = 16) -> tuple[int, int]:
+    """Output columns of a column-parallel shard (16-column panels)."""
+    if N % align:
+        return even_split(N, world, rank)
+    lo, hi = even_split(N // align, world, rank)
+    return lo * align, hi * align
+
+
+# ---------------------------------------------------------------------------
+# process group wrapper
+# ---------------------------------------------------------------------------
+
+class TP:
+    """Rank/world of the tensor-parallel group (torch.distributed or single)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.group = group
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+
+    def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def all_gather_cat(self, t: torch.Tensor, sizes: list[int]) -> torch.Tensor:
+        """Concatenate per-rank last-dim slices (uneven sizes padded)."""
+        if self.world == 1:
+            return t
+        mx = max(sizes)
+        pad = F.pad(t, (0, mx - t.shape[-1]))
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(outs, pad.contiguous(), group=self.group)
+        return torch.cat([o[..., :s] for o, s in zip(outs, sizes)], dim=-1)
+
+
+# ---------------------------------------------------------------------------
+# linear backends
+# ---------------------------------------------------------------------------
+
+class GpuLinear:
+    """Quantized linear on the B200 GEMV: W [K, N] quantized on the GPU."""
+
+    def __init__(self, w: torch.Tensor, qcfg: QuantConfig):
+        self.pw = PanelWeights.from_float(w, qcfg)
+        self.K, self.N = w.shape
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None,
+                 accumulate: bool = False) -> torch.Tensor:
+        return self.pw.gemv(x, out=out, accumulate=accumulate)
+
+    @property
+    def nbytes(self) -> int:
+        return self.pw.nbytes_algorithmic()
+
+
+class GpuBackend:
+    linear = GpuLinear
+
+
+# ---------------------------------------------------------------------------
+# the model
+# ---------------------------------------------------------------------------
+
+def _rmsnorm(h: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    var = h.pow(2).mean(-1, keepdim=True)
+    return h * torch.rsqrt(var + eps) * w
+
+
+def _rope(t: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    """Rotary embedding on [B, H, hd] (rotate-half convention)."""
+    h = t.shape[-1] // 2
+    t1, t2 = t[..., :h], t[..., h:]
+    return torch.cat([t1 * cos - t2 * sin, t2 * cos + t1 * sin], dim=-1)
+
+
+class LlamaTP:
+    """One tensor-parallel shard of a random-init LLaMA-architecture model."""
+
+    def __init__(self, cfg: LlamaConfig, *, batch: int = 1, max_ctx: int = 1024, seed: int = 0,
+                 device=None, tp: TP | None = None, backend=GpuBackend,
+                 kv_dtype=torch.float16):
+        self.cfg, self.B, self.max_ctx = cfg, batch, max_ctx
+        self.tp = tp or TP()
+        self.dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.backend = backend
+        r, w = self.tp.rank, self.tp.world
+        d, hd = cfg.d_model, cfg.head_dim
+        self.h0, self.h1 = head_shard(cfg.n_heads, w, r)
+        self.nh = self.h1 - self.h0
+        # FFN columns: also the K-shard of down_proj, so whole groups/supersteps
+        self.f0, self.f1 = row_shard(cfg.ffn, cfg.group, w, r)
+        self.nf = self.f1 - self.f0
+        self.v_sizes = [col_shard(cfg.vocab, w, q)[1] - col_shard(cfg.vocab, w, q)[0]
+                        for q in range(w)]
+        self.v0, self.v1 = col_shard(cfg.vocab, w, r)
+        # o_proj / down_proj K-shards: heads / FFN columns of this rank
+        self.o_rows = (self.h0 * hd, self.h1 * hd)
+        self.d_rows = (self.f0, self.f1)
+        gen = torch.Generator(device=self.dev)
+
+        def randn(shape, tag):
+            gen.manual_seed(seed * 1_000_003 + tag)
+            return torch.randn(shape, generator=gen, device=self.dev) * 0.02
+
+        self.layers = []
+        for li in range(cfg.n_layers):
+            base = 100 * li
+            # column-parallel fused QKV: global W_q|W_k|W_v [d, 3 d]; this rank's heads
+            wq, wk, wv = (randn((d, cfg.n_heads * hd), base + i) for i in range(3))
+            sl = slice(self.h0 * hd, self.h1 * hd)
+            wqkv = torch.cat([wq[:, sl], wk[:, sl], wv[:, sl]], dim=1).contiguous()
+            del wq, wk, wv
+            wo = randn((cfg.n_heads * hd, d), base + 3)[self.o_rows[0]:self.o_rows[1]].contiguous()
+            wg = randn((d, cfg.ffn), base + 4)[:, self.f0:self.f1]
+            wu = randn((d, cfg.ffn), base + 5)[:, self.f0:self.f1]
+            wgu = torch.cat([wg, wu], dim=1).contiguous()
+            del wg, wu
+            wd = randn((cfg.ffn, d), base + 6)[self.d_rows[0]:self.d_rows[1]].contiguous()
+            layer = {
+                "qkv": backend.linear(wqkv, cfg.qcfg),
+                "o": backend.linear(wo, cfg.qcfg),
+                "gu": backend.linear(wgu, cfg.qcfg),
+                "down": backend.linear(wd, cfg.qcfg),
+                "n1": torch.ones(d, device=self.dev),
+                "n2": torch.ones(d, device=self.dev),
+            }
+            del wqkv, wo, wgu, wd
+            self.layers.append(layer)
+        self.norm = torch.ones(d, device=self.dev)
+        gen.manual_seed(seed * 1_000_003 + 999_999)
+        self.embed = (torch.randn((cfg.vocab, d), generator=gen, device=self.dev) * 0.02).half()
+        gen.manual_seed(seed * 1_000_003 + 999_998)
+        self.lm_head = (torch.randn((d, cfg.vocab), generator=gen, device=self.dev)
+                        * 0.02)[:, self.v0:self.v1].half().t().contiguous()  # [V_l, d]
+        # synthetic fp16 KV cache [layer][B, H_l, ctx, hd]: slices of one global
+        # cache per layer, so every TP degree sees the same past tokens
+        kshape = (cfg.n_layers, batch, self.nh, max_ctx, hd)
+        self.k_cache = torch.empty(kshape, dtype=kv_dtype, device=self.dev)
+        self.v_cache = torch.empty(kshape, dtype=kv_dtype, device=self.dev)
+        for li in range(cfg.n_layers):
+            for j, cache in enumerate((self.k_cache, self.v_cache)):
+                g = randn((batch, cfg.n_heads, max_ctx, hd), 10_000_000 + 2 * li + j) * 50.0
+                cache[li] = g[:, self.h0:self.h1].to(kv_dtype)
+                del g
+        inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device=self.dev).float() / hd))
+        ang = torch.arange(max_ctx, device=self.dev).float()[:, None] * inv[None, :]
+        self.cos, self.sin = ang.cos(), ang.sin()  # [ctx, hd/2]
+
+    # -- accounting ---------------------------------------------------------
+    def weight_bytes(self) -> int:
+        """Algorithmic bytes of the quantized linears of this shard."""
+        return sum(lay[k].nbytes for lay in self.layers for k in ("qkv", "o", "gu", "down"))
+
+    def bytes_per_step(self, pos: int) -> int:
+        """HBM bytes one decode step must read on this shard: quantized weights
+        (codes + f32 scale/zero), fp16 lm_head shard, KV cache up to pos."""
+        kv = 2 * self.cfg.n_layers * self.B * self.nh * (pos + 1) * self.cfg.head_dim * 2
+        return self.weight_bytes() + self.lm_head.numel() * 2 + kv
+
+    # -- one decode step ----------------------------------------------------
+    def step(self, tokens: torch.Tensor, pos: int) -> torch.Tensor:
+        """Greedy next tokens for `tokens` [B] at position `pos` (static shapes:
+        graph-capturable for a fixed pos)."""
+        cfg, B, hd = self.cfg, self.B, self.cfg.head_dim
+        h = self.embed[tokens].float()                     # [B, d]
+        cos, sin = self.cos[pos], self.sin[pos]
+        scale = 1.0 / math.sqrt(hd)
+        for li, lay in enumerate(self.layers):
+            xn = _rmsnorm(h, lay["n1"], cfg.norm_eps)
+            qkv = lay["qkv"](xn)                           # [B, 3 H_l hd]
+            q, k, v = qkv.view(B, 3, self.nh, hd).unbind(1)
+            q, k = _rope(q, cos, sin), _rope(k, cos, sin)
+            self.k_cache[li, :, :, pos] = k.to(self.k_cache.dtype)
+            self.v_cache[li, :, :, pos] = v.to(self.v_cache.dtype)
+            kc = self.k_cache[li, :, :, : pos + 1]
+            vc = self.v_cache[li, :, :, : pos + 1]
+            att = F.scaled_dot_product_attention(q.to(kc.dtype).unsqueeze(2), kc, vc,
+                                                 scale=scale)  # [B, H_l, 1, hd]
+            att = att.reshape(B, self.nh * hd).float()
+            # row-parallel o_proj: rank 0 folds the residual into its partial
+            h = self._row_parallel(lay["o"], att, h)
+            xn = _rmsnorm(h, lay["n2"], cfg.norm_eps)
+            gu = lay["gu"](xn)                             # [B, 2 F_l]
+            act = F.silu(gu[:, : self.nf]) * gu[:, self.nf:]
+            h = self._row_parallel(lay["down"], act, h)
+        xn = _rmsnorm(h, self.norm, cfg.norm_eps).half()
+        logits = (xn @ self.lm_head.t()).float()           # [B, V_l]
+        logits = self.tp.all_gather_cat(logits, self.v_sizes)
+        self.last_logits = logits
+        return logits.argmax(-1)
+
+    def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor) -> torch.Tensor:
+        if self.tp.rank == 0:
+            out = h.clone()
+            lin(x, out=out, accumulate=True)               # h + partial_0
+        else:
+            out = lin(x)                                   # partial_r
+        return self.tp.all_reduce(out)
+
+
+def shrink(cfg: LlamaConfig, **kw) -> LlamaConfig:
+    return replace(cfg, **kw)

@@ -41,3 +41,7 @@ def golden_plans():
 @pytest.fixture(scope="session")
 def golden_kats():
     return json.loads((GOLDEN / "kats.json").read_text())
+
+TESTS = Path(__file__).resolve().parent
+if str(TESTS) not in sys.path:
+    sys.path.insert(0, str(TESTS))

@@ -1,0 +1,87 @@
+"""Tensor-parallel decode driver: shard arithmetic, and TP=2 (gloo, CPU) against
+TP=1 on a tiny LLaMA-architecture model with the oracle linear backend."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2307_03738_b200 import decode as D
+
+
+def test_row_shards_are_group_and_superstep_aligned():
+    # 7B down_proj: K = 11008 = 43 supersteps of 256 -> uneven at TP 2/4/8
+    for world in (1, 2, 4, 8):
+        cuts = [D.row_shard(11008, 128, world, r) for r in range(world)]
+        assert cuts[0][0] == 0 and cuts[-1][1] == 11008
+        assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+        assert all((hi - lo) % 256 == 0 for lo, hi in cuts)
+        sizes = [hi - lo for lo, hi in cuts]
+        assert max(sizes) - min(sizes) <= 256
+    # 65B: K = 22016 = 344 groups of 64 = 86 supersteps
+    for world in (2, 4, 8):
+        cuts = [D.row_shard(22016, 64, world, r) for r in range(world)]
+        assert sum(hi - lo for lo, hi in cuts) == 22016
+        assert all((hi - lo) % 64 == 0 for lo, hi in cuts)
+    with pytest.raises(ValueError):
+        D.row_shard(4096, None, 2, 0)
+
+
+def test_head_and_vocab_shards():
+    assert [D.head_shard(32, 8, r) for r in range(2)] == [(0, 4), (4, 8)]
+    with pytest.raises(ValueError):
+        D.head_shard(64, 3, 0)
+    cuts = [D.col_shard(32000, 8, r) for r in range(8)]
+    assert cuts[-1][1] == 32000 and all((hi - lo) % 16 == 0 for lo, hi in cuts)
+
+
+TINY = D.LlamaConfig(n_layers=2, d_model=128, n_heads=4, head_dim=32, ffn=512, vocab=160,
+                     bits=4, group=32)
+
+
+def _run(rank, world, port, q):
+    from decode_backends import OracleBackend
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.manual_seed(0)
+    m = D.LlamaTP(TINY, batch=2, max_ctx=16, seed=3, device="cpu", tp=D.TP(),
+                  backend=OracleBackend, kv_dtype=torch.float32)
+    tok = m.step(torch.tensor([5, 17]), pos=8)
+    if rank == 0:
+        q.put((tok.tolist(), m.last_logits.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_tp2_matches_tp1_on_cpu():
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from decode_backends import OracleBackend
+    ref = D.LlamaTP(TINY, batch=2, max_ctx=16, seed=3, device="cpu", backend=OracleBackend,
+                    kv_dtype=torch.float32)
+    tok1 = ref.step(torch.tensor([5, 17]), pos=8)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    tok2, logits2 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    l1 = ref.last_logits.numpy()
+    assert tok2 == tok1.tolist()
+    assert abs(logits2 - l1).max() / (1 + abs(l1).max()) < 1e-5
