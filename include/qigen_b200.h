@@ -108,6 +108,27 @@ int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int b
                int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
                float* y, int64_t ldy, int accumulate, int k_splits, void* stream);
 
+/* qigen_gemv with a fused activation prologue (the decode driver's glue):
+ *   prologue 0: x as given;
+ *   prologue 1: RMSNorm, x_k * rsqrt(mean_k(x^2) + eps) * prologue_w[k] (LLaMA RMSNorm);
+ *   prologue 2: SwiGLU, silu(x[t, k]) * x[t, n + k] (x holds gate | up, ldx >= 2n). */
+int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+                  int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
+                  float* y, int64_t ldy, int accumulate, int k_splits, int prologue,
+                  const float* prologue_w, float eps, void* stream);
+
+/* ---- decode-step glue (LLaMA driver) ----------------------------------------- */
+
+/* RoPE on q and k of a fused QKV output qkv f32 [B, 3, H, hd] at position pos
+ * (cos/sin: [hd/2] for that position); q -> f16 [B, H, hd]; k, v appended (f16)
+ * to the layer's caches [B, H, ctx, hd] at pos. */
+int qigen_rope_kv(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
+                  const float* cos_pos, const float* sin_pos, void* q_out, void* k_cache,
+                  void* v_cache, int64_t ctx, int64_t pos, void* stream);
+/* out f16 [rows, d] = h * rsqrt(mean(h^2) + eps) * w. */
+int qigen_rmsnorm_f16(const float* h, const float* w, int64_t rows, int64_t d, float eps,
+                      void* out, void* stream);
+
 /* Debugging aid: when buf is non-NULL every later qigen_gemv launch writes
  * %globaltimer stamps (entry, after the PDL wait, after the activation
  * prologue, after the main loop, exit) to buf[(cta_y*grid_x + cta_x)*8 + i]. */

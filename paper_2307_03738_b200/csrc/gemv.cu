@@ -51,6 +51,9 @@ struct GemvArgs {
   int max_steps;     // max K-steps (32 rows) of any chunk
   int D;             // ring stages per warp
   int pre;           // stages per warp issued before griddepcontrol.wait
+  int xmode;         // activation prologue: 0 plain, 1 RMSNorm(x) * w, 2 SwiGLU(x[:n], x[n:])
+  const float* xw;   // RMSNorm weight [n]
+  float eps;         // RMSNorm epsilon
   unsigned long long* trace;  // optional per-CTA timestamps (qigen_debug_trace)
 };
 
@@ -176,9 +179,9 @@ struct RowScale {  // scale of the rows gq+8 accumulators relative to rows gq
 
 __device__ __forceinline__ int sbyte(int v) { return (int)(int8_t)(v & 0xFF); }
 
-// Four consecutive activations as f32 (zero beyond n).
-__device__ __forceinline__ void load_x4(const GemvArgs& a, int tk, int64_t k, float (&v)[4]) {
-  const int64_t base = tk * a.ldx + k;
+// Four consecutive raw activations (row element offset `base`, `k` = column) as
+// f32, zero beyond n.
+__device__ __forceinline__ void load_raw4(const GemvArgs& a, int64_t base, int64_t k, float (&v)[4]) {
   if (a.x_vec && k + 3 < a.n) {
     if (a.x_dtype == QIGEN_F32) {
       const float4 f = __ldg((const float4*)((const float*)a.x + base));
@@ -208,9 +211,26 @@ __device__ __forceinline__ void load_x4(const GemvArgs& a, int tk, int64_t k, fl
   }
 }
 
+// Four consecutive GEMV inputs after the fused prologue transform:
+//   xmode 0: x;  1: x * inv_rms(token) * w (RMSNorm);  2: silu(x[k]) * x[n + k] (SwiGLU)
+__device__ __forceinline__ void load_x4(const GemvArgs& a, int tk, int64_t k, float (&v)[4],
+                                        const float* inv_rms) {
+  load_raw4(a, tk * a.ldx + k, k, v);
+  if (a.xmode == 1) {
+    const float inv = inv_rms[tk];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (k + i < a.n) ? v[i] * inv * __ldg(a.xw + k + i) : 0.f;
+  } else if (a.xmode == 2) {
+    float u[4];
+    load_raw4(a, tk * a.ldx + a.n + k, k, u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = v[i] / (1.f + __expf(-v[i])) * u[i];
+  }
+}
+
 // Shared-memory carve-up (bytes), identical on host and device.
 struct SmemLayout {
-  int ring, bars, bfrag, xu, su, zero, rbar, yp, total, stage;
+  int ring, bars, bfrag, xu, su, zero, rbar, inv, yp, total, stage;
   __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int M, int WPC, int S) {
     stage = bits * 512 + szb;
     const int max_units = max_steps;  // units are >= 32 rows
@@ -222,6 +242,7 @@ struct SmemLayout {
     su = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
     zero = off;  off += 8;
     rbar = off;  off += 8;
+    inv = off;   off += 16 * 4;
     yp = off;    off += (S - 1) * WPC * 16 * M * 4 + 16;  // owner's inbox
     total = off;
   }
@@ -291,10 +312,14 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   // the point of coherence, and nothing is read into registers or L1 here)
   {
     const int esz = a.x_dtype == QIGEN_F32 ? 4 : 2;
-    const int64_t kb = (int64_t)ks0 * kSuper * esz, ke = min((int64_t)ks1 * kSuper, a.n) * esz;
+    const int64_t kb = a.xmode == 1 ? 0 : (int64_t)ks0 * kSuper * esz;
+    const int64_t ke = (a.xmode == 1 ? a.n : min((int64_t)ks1 * kSuper, a.n)) * esz;
     const int lines = (int)((ke - kb + 127) / 128);
-    for (int i = threadIdx.x; i < lines * M; i += T) {
-      const char* pa = (const char*)a.x + (i / lines) * a.ldx * esz + kb + (int64_t)(i % lines) * 128;
+    const int halves = a.xmode == 2 ? 2 : 1;
+    for (int i = threadIdx.x; i < lines * M * halves; i += T) {
+      const int li = i % lines, rest = i / lines;
+      const char* pa = (const char*)a.x + ((rest % M) * a.ldx + (rest / M) * a.n) * esz + kb +
+                       (int64_t)li * 128;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
     }
   }
@@ -305,6 +330,28 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   trace_point(a, 1);
 
   // ---- 3. activation prologue: per-unit exponent, digits, unit sums ---------
+  float* inv_rms = (float*)(smem + L.inv);
+  if (a.xmode == 1) {  // fused RMSNorm: every CTA reduces the full rows (L2 hits)
+    float* red = xu;  // scratch: the unit sums are written only after this pass
+    for (int tk = 0; tk < M; ++tk) {
+      float ss = 0.f;
+      for (int64_t k = 4 * threadIdx.x; k < a.n; k += 4 * T) {
+        float v[4];
+        load_raw4(a, tk * a.ldx + k, k, v);
+        ss += v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) red[tk * WPC + warp] = ss;
+    }
+    __syncthreads();
+    if (threadIdx.x < M) {
+      float ss = 0.f;
+      for (int w = 0; w < WPC; ++w) ss += red[threadIdx.x * WPC + w];
+      inv_rms[threadIdx.x] = rsqrtf(ss / (float)a.n + a.eps);
+    }
+    __syncthreads();
+  }
   {
     const int64_t k0 = (int64_t)ks0 * kSuper;
     const int items = M * nsteps * 8;  // item = (token, step, half, t): 4 consecutive k
@@ -321,7 +368,7 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
         v[r][0] = v[r][1] = v[r][2] = v[r][3] = 0.f;
         if (it < items) {
           const int sub = it & 7, st = (it >> 3) % nsteps, tk = (it >> 3) / nsteps;
-          load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v[r]);
+          load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v[r], inv_rms);
         }
       }
       if (first) {  // the rest of the first ring fill goes out behind the x loads
@@ -655,9 +702,10 @@ extern "C" int qigen_debug_prefetch(int stages_before_wait) {
   g_pre = stages_before_wait;
   return QIGEN_OK;
 }
-extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
-                          int64_t group, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
-                          float* y, int64_t ldy, int accumulate, int k_splits, void* stream) {
+extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+                             int64_t group, const void* x, int x_dtype, int64_t tokens,
+                             int64_t ldx, float* y, int64_t ldy, int accumulate, int k_splits,
+                             int prologue, const float* prologue_w, float eps, void* stream) {
   QIGEN_CHECK_ARG(bits == 2 || bits == 3 || bits == 4, QIGEN_ERR_CONFIG,
                   "bits must be one of (2, 3, 4), got %d", bits);
   QIGEN_CHECK_ARG(qw && qsz && x && y, QIGEN_ERR_ARG, "null pointer");
@@ -671,7 +719,10 @@ extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64
   QIGEN_CHECK_ARG(tokens >= 1 && tokens <= 16, QIGEN_ERR_UNSUPPORTED,
                   "the GEMV path takes 1..16 activation rows, got %lld", (long long)tokens);
   QIGEN_CHECK_ARG(x_dtype >= 0 && x_dtype <= 2, QIGEN_ERR_ARG, "bad x dtype %d", x_dtype);
-  QIGEN_CHECK_ARG(ldx >= n && ldy >= m, QIGEN_ERR_ARG, "leading dimensions too small");
+  QIGEN_CHECK_ARG(prologue >= 0 && prologue <= 2, QIGEN_ERR_ARG, "bad prologue %d", prologue);
+  QIGEN_CHECK_ARG(prologue != 1 || prologue_w, QIGEN_ERR_ARG, "RMSNorm prologue needs a weight");
+  QIGEN_CHECK_ARG(ldx >= (prologue == 2 ? 2 * n : n) && ldy >= m, QIGEN_ERR_ARG,
+                  "leading dimensions too small");
   QIGEN_CHECK_ARG(k_splits >= 0 && k_splits <= kMaxSplits, QIGEN_ERR_ARG,
                   "k_splits %d out of range", k_splits);
   GemvArgs a = {};
@@ -690,7 +741,10 @@ extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64
   a.M = (int)tokens;
   a.x_dtype = x_dtype;
   const int esz = x_dtype == QIGEN_F32 ? 4 : 2;
-  a.x_vec = ((uintptr_t)x % 16 == 0) && ((ldx * esz) % 16 == 0);
+  a.x_vec = ((uintptr_t)x % 16 == 0) && ((ldx * esz) % 16 == 0) && ((n * esz) % 16 == 0 || prologue != 2);
+  a.xmode = prologue;
+  a.xw = prologue_w;
+  a.eps = eps;
   a.accumulate = accumulate;
   a.trace = g_trace;
   const int S = k_splits;  // 0: chosen per launch shape in launch_cfg
@@ -702,4 +756,11 @@ extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64
     default: QIGEN_LAUNCH(4);
   }
 #undef QIGEN_LAUNCH
+}
+
+extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+                          int64_t group, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
+                          float* y, int64_t ldy, int accumulate, int k_splits, void* stream) {
+  return qigen_gemv_ex(qw, qsz, n, m, bits, group, x, x_dtype, tokens, ldx, y, ldy, accumulate,
+                       k_splits, 0, nullptr, 0.f, stream);
 }

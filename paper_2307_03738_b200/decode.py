@@ -30,6 +30,8 @@ from dataclasses import dataclass, replace
 import torch
 import torch.nn.functional as F
 
+from . import _dev
+from ._lib import call
 from .config import QuantConfig
 from .runtime import PanelWeights
 
@@ -138,9 +140,10 @@ class GpuLinear:
         self.pw = PanelWeights.from_float(w, qcfg)
         self.K, self.N = w.shape
 
-    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None,
-                 accumulate: bool = False) -> torch.Tensor:
-        return self.pw.gemv(x, out=out, accumulate=accumulate)
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,
+                 prologue: str | None = None, norm_weight=None, eps: float = 1e-5) -> torch.Tensor:
+        return self.pw.gemv(x, out=out, accumulate=accumulate, prologue=prologue,
+                            norm_weight=norm_weight, eps=eps)
 
     @property
     def nbytes(self) -> int:
@@ -148,24 +151,26 @@ class GpuLinear:
 
 
 class GpuBackend:
+    """The product backend: every op is a libqigen_b200 kernel (no fallback)."""
+
     linear = GpuLinear
+
+    @staticmethod
+    def rope_kv(qkv, cos, sin, q_out, k_cache, v_cache, pos):
+        B, H, ctx, hd = k_cache.shape
+        call("qigen_rope_kv", qkv.data_ptr(), B, H, hd, cos.data_ptr(), sin.data_ptr(),
+             q_out.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), ctx, pos,
+             _dev.stream_handle())
+
+    @staticmethod
+    def rmsnorm_f16(h, w, eps, out):
+        call("qigen_rmsnorm_f16", h.data_ptr(), w.data_ptr(), h.shape[0], h.shape[1], float(eps),
+             out.data_ptr(), _dev.stream_handle())
 
 
 # ---------------------------------------------------------------------------
 # the model
 # ---------------------------------------------------------------------------
-
-def _rmsnorm(h: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
-    var = h.pow(2).mean(-1, keepdim=True)
-    return h * torch.rsqrt(var + eps) * w
-
-
-def _rope(t: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
-    """Rotary embedding on [B, H, hd] (rotate-half convention)."""
-    h = t.shape[-1] // 2
-    t1, t2 = t[..., :h], t[..., h:]
-    return torch.cat([t1 * cos - t2 * sin, t2 * cos + t1 * sin], dim=-1)
-
 
 class LlamaTP:
     """One tensor-parallel shard of a random-init LLaMA-architecture model."""
@@ -254,41 +259,40 @@ class LlamaTP:
     # -- one decode step ----------------------------------------------------
     def step(self, tokens: torch.Tensor, pos: int) -> torch.Tensor:
         """Greedy next tokens for `tokens` [B] at position `pos` (static shapes:
-        graph-capturable for a fixed pos)."""
-        cfg, B, hd = self.cfg, self.B, self.cfg.head_dim
-        h = self.embed[tokens].float()                     # [B, d]
+        graph-capturable for a fixed pos).  Per layer: QKV GEMV (RMSNorm fused
+        into its prologue) -> RoPE + KV append -> attention -> o_proj GEMV
+        (residual fused, all-reduce) -> gate|up GEMV (RMSNorm fused) -> down
+        GEMV (SwiGLU fused, residual fused, all-reduce)."""
+        cfg, B, hd, be = self.cfg, self.B, self.cfg.head_dim, self.backend
+        h = self.embed[tokens].float()                     # [B, d] residual stream
         cos, sin = self.cos[pos], self.sin[pos]
+        q16 = torch.empty((B, self.nh, 1, hd), dtype=self.k_cache.dtype, device=self.dev)
         scale = 1.0 / math.sqrt(hd)
         for li, lay in enumerate(self.layers):
-            xn = _rmsnorm(h, lay["n1"], cfg.norm_eps)
-            qkv = lay["qkv"](xn)                           # [B, 3 H_l hd]
-            q, k, v = qkv.view(B, 3, self.nh, hd).unbind(1)
-            q, k = _rope(q, cos, sin), _rope(k, cos, sin)
-            self.k_cache[li, :, :, pos] = k.to(self.k_cache.dtype)
-            self.v_cache[li, :, :, pos] = v.to(self.v_cache.dtype)
+            qkv = lay["qkv"](h, prologue="rmsnorm", norm_weight=lay["n1"], eps=cfg.norm_eps)
+            be.rope_kv(qkv, cos, sin, q16, self.k_cache[li], self.v_cache[li], pos)
             kc = self.k_cache[li, :, :, : pos + 1]
             vc = self.v_cache[li, :, :, : pos + 1]
-            att = F.scaled_dot_product_attention(q.to(kc.dtype).unsqueeze(2), kc, vc,
-                                                 scale=scale)  # [B, H_l, 1, hd]
-            att = att.reshape(B, self.nh * hd).float()
-            # row-parallel o_proj: rank 0 folds the residual into its partial
-            h = self._row_parallel(lay["o"], att, h)
-            xn = _rmsnorm(h, lay["n2"], cfg.norm_eps)
-            gu = lay["gu"](xn)                             # [B, 2 F_l]
-            act = F.silu(gu[:, : self.nf]) * gu[:, self.nf:]
-            h = self._row_parallel(lay["down"], act, h)
-        xn = _rmsnorm(h, self.norm, cfg.norm_eps).half()
+            att = F.scaled_dot_product_attention(q16, kc, vc, scale=scale)  # [B, H_l, 1, hd]
+            h = self._row_parallel(lay["o"], att.reshape(B, self.nh * hd), h)
+            gu = lay["gu"](h, prologue="rmsnorm", norm_weight=lay["n2"], eps=cfg.norm_eps)
+            h = self._row_parallel(lay["down"], gu, h, prologue="swiglu")
+        xn = torch.empty((B, cfg.d_model), dtype=torch.float16, device=self.dev)
+        be.rmsnorm_f16(h, self.norm, cfg.norm_eps, xn)
         logits = (xn @ self.lm_head.t()).float()           # [B, V_l]
         logits = self.tp.all_gather_cat(logits, self.v_sizes)
         self.last_logits = logits
         return logits.argmax(-1)
 
-    def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor) -> torch.Tensor:
+    def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor, prologue=None) -> torch.Tensor:
+        """Row-parallel linear + residual: rank 0 accumulates its partial into h
+        inside the GEMV epilogue, the other ranks produce bare partials, and one
+        all-reduce forms h + sum of partials on every rank."""
         if self.tp.rank == 0:
-            out = h.clone()
-            lin(x, out=out, accumulate=True)               # h + partial_0
+            lin(x, out=h, accumulate=True, prologue=prologue)
+            out = h
         else:
-            out = lin(x)                                   # partial_r
+            out = lin(x, prologue=prologue)
         return self.tp.all_reduce(out)
 
 

@@ -133,12 +133,22 @@ class PanelWeights:
         return self.n * self.m * self.bits // 8 + G * self.m * 8
 
     def gemv(self, x: torch.Tensor, out: torch.Tensor | None = None, *, accumulate: bool = False,
-             k_splits: int = 0) -> torch.Tensor:
-        """y[t, :] = x[t, :] @ W for t < tokens; x: CUDA [tokens, n] or [n]."""
+             k_splits: int = 0, prologue: str | None = None, norm_weight: torch.Tensor | None = None,
+             eps: float = 1e-5) -> torch.Tensor:
+        """y[t, :] = f(x[t, :]) @ W for t < tokens; x: CUDA [tokens, n] or [n].
+
+        ``prologue`` fuses the producer-side glue into the GEMV: None (f = id),
+        ``"rmsnorm"`` (f = RMSNorm with ``norm_weight``) or ``"swiglu"`` (x holds
+        gate | up, [tokens, 2n]; f = silu(gate) * up)."""
         squeeze = x.dim() == 1
         x2 = x.reshape(1, -1) if squeeze else x
-        if x2.dim() != 2 or x2.shape[1] != self.n:
-            raise ConfigError(f"x has shape {tuple(x.shape)}, expected [..., {self.n}]")
+        width = 2 * self.n if prologue == "swiglu" else self.n
+        if x2.dim() != 2 or x2.shape[1] != width:
+            raise ConfigError(f"x has shape {tuple(x.shape)}, expected [..., {width}]")
+        mode = {None: 0, "rmsnorm": 1, "swiglu": 2}[prologue]
+        if mode == 1 and (norm_weight is None or norm_weight.dtype != torch.float32
+                          or not norm_weight.is_cuda or norm_weight.numel() != self.n):
+            raise ConfigError("rmsnorm prologue needs a float32 CUDA weight of length n")
         if x2.dtype not in _DTYPES:
             x2 = x2.float()
         if x2.stride(1) != 1:
@@ -154,9 +164,10 @@ class PanelWeights:
         for t0 in range(0, T, MAX_GEMV_TOKENS):
             t1 = min(T, t0 + MAX_GEMV_TOKENS)
             xs, ys = x2[t0:t1], y2[t0:t1]
-            call("qigen_gemv", self.qw.data_ptr(), self.qsz.data_ptr(), self.n, self.m, self.bits,
-                 self.group_code, xs.data_ptr(), _DTYPES[xs.dtype], t1 - t0, xs.stride(0),
-                 ys.data_ptr(), ys.stride(0), int(accumulate), int(k_splits), st)
+            call("qigen_gemv_ex", self.qw.data_ptr(), self.qsz.data_ptr(), self.n, self.m,
+                 self.bits, self.group_code, xs.data_ptr(), _DTYPES[xs.dtype], t1 - t0,
+                 xs.stride(0), ys.data_ptr(), ys.stride(0), int(accumulate), int(k_splits), mode,
+                 norm_weight.data_ptr() if mode == 1 else None, float(eps), st)
         return out.reshape(self.m) if squeeze else out
 
 

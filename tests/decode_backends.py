@@ -16,7 +16,15 @@ class OracleLinear:
         self.wd = torch.from_numpy(orc.dequantize_matrix(codes, s, z).astype(np.float64))
         self.K, self.N = wn.shape
 
-    def __call__(self, x, out=None, accumulate=False):
+    def __call__(self, x, out=None, accumulate=False, prologue=None, norm_weight=None, eps=1e-5):
+        x = x.float()
+        if prologue == "rmsnorm":
+            x = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * norm_weight
+        elif prologue == "swiglu":
+            n = x.shape[-1] // 2
+            x = torch.nn.functional.silu(x[..., :n]) * x[..., n:]
+        if self.wd.device != x.device:
+            self.wd = self.wd.to(x.device)
         y = (x.double() @ self.wd).float()
         if out is None:
             return y
@@ -33,3 +41,20 @@ class OracleLinear:
 
 class OracleBackend:
     linear = OracleLinear
+
+    @staticmethod
+    def rope_kv(qkv, cos, sin, q_out, k_cache, v_cache, pos):
+        B, H, ctx, hd = k_cache.shape
+        q, k, v = qkv.view(B, 3, H, hd).unbind(1)
+        half = hd // 2
+
+        def rot(t):
+            return torch.cat([t[..., :half] * cos - t[..., half:] * sin,
+                              t[..., half:] * cos + t[..., :half] * sin], dim=-1)
+        q_out.copy_(rot(q).view_as(q_out))
+        k_cache[:, :, pos] = rot(k).to(k_cache.dtype)
+        v_cache[:, :, pos] = v.to(v_cache.dtype)
+
+    @staticmethod
+    def rmsnorm_f16(h, w, eps, out):
+        out.copy_(h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + eps) * w)
