@@ -111,11 +111,16 @@ int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int b
 /* qigen_gemv with a fused activation prologue (the decode driver's glue):
  *   prologue 0: x as given;
  *   prologue 1: RMSNorm, x_k * rsqrt(mean_k(x^2) + eps) * prologue_w[k] (LLaMA RMSNorm);
- *   prologue 2: SwiGLU, silu(x[t, k]) * x[t, n + k] (x holds gate | up, ldx >= 2n). */
+ *   prologue 2: SwiGLU, silu(x[t, k]) * x[t, n + k] (x holds gate | up, ldx >= 2n).
+ * workspace (device, >= qigen_gemv_workspace_size bytes, or NULL): scratch for the
+ * activation digits when they are prepared once per call (long K chunks / many
+ * tokens); NULL uses a grow-only library buffer that cannot grow during capture. */
+int64_t qigen_gemv_workspace_size(int64_t n, int64_t tokens);
 int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
                   int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
                   float* y, int64_t ldy, int accumulate, int k_splits, int prologue,
-                  const float* prologue_w, float eps, void* stream);
+                  const float* prologue_w, float eps, void* workspace, int64_t workspace_bytes,
+                  void* stream);
 
 /* ---- decode-step glue (LLaMA driver) ----------------------------------------- */
 
@@ -131,11 +136,13 @@ int qigen_rmsnorm_f16(const float* h, const float* w, int64_t rows, int64_t d, f
 
 /* Debugging aid: when buf is non-NULL every later qigen_gemv launch writes
  * %globaltimer stamps (entry, after the PDL wait, after the activation
- * prologue, after the main loop, exit) to buf[(cta_y*grid_x + cta_x)*8 + i]. */
+ * prologue, after the main loop, exit, ...) to buf[(cta_y*grid_x + cta_x)*16 + i]. */
 int qigen_debug_trace(void* buf);
 /* Tuning aid: weight stages per warp issued before griddepcontrol.wait
  * (-1 = the whole first ring fill, the default). */
 int qigen_debug_prefetch(int stages_before_wait);
+/* Tuning aid: 1 = always digitise activations in the separate prep kernel. */
+int qigen_debug_force_prep(int on);
 
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
 

@@ -48,12 +48,14 @@ SIGNATURES = {
     "qigen_input_sums": (_I32, [_P, _I64, _I64, _P, _P]),
     "qigen_gemv": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64,
                           _I32, _I32, _P]),
+    "qigen_gemv_workspace_size": (_I64, [_I64, _I64]),
     "qigen_gemv_ex": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64,
-                             _I32, _I32, _I32, _P, ctypes.c_float, _P]),
+                             _I32, _I32, _I32, _P, ctypes.c_float, _P, _I64, _P]),
     "qigen_rope_kv": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "qigen_rmsnorm_f16": (_I32, [_P, _P, _I64, _I64, ctypes.c_float, _P, _P]),
     "qigen_debug_trace": (_I32, [_P]),
     "qigen_debug_prefetch": (_I32, [_I32]),
+    "qigen_debug_force_prep": (_I32, [_I32]),
     "qigen_weights_create": (_I32, [_P, _I32, _I64, _I64, _I32, _I64, _I64, _I64, _P, _I64,
                                     _P, _P, _P, ctypes.POINTER(_P)]),
     "qigen_weights_destroy": (_I32, [_P]),

@@ -30,6 +30,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <unordered_map>
+#include <utility>
 
 #include "common.cuh"
 
@@ -54,6 +56,9 @@ struct GemvArgs {
   int xmode;         // activation prologue: 0 plain, 1 RMSNorm(x) * w, 2 SwiGLU(x[:n], x[n:])
   const float* xw;   // RMSNorm weight [n]
   float eps;         // RMSNorm epsilon
+  unsigned char* dig;         // prepared activation digits (act_prep_kernel) or null
+  unsigned char* ws;          // caller workspace for `dig` (may be null)
+  size_t ws_bytes;
   unsigned long long* trace;  // optional per-CTA timestamps (qigen_debug_trace)
 };
 
@@ -61,7 +66,7 @@ __device__ __forceinline__ void trace_point(const GemvArgs& a, int i) {
   if (a.trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = t;
+    a.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + i] = t;
   }
 }
 
@@ -228,20 +233,139 @@ __device__ __forceinline__ void load_x4(const GemvArgs& a, int tk, int64_t k, fl
   }
 }
 
+// ---- activation digitisation (shared by the fused prologue and the prep kernel)
+// An "item" is 4 consecutive rows of one token.  IPU consecutive lanes hold one
+// exponent unit (U = min(g, 128) rows); they agree on E (max |x| < 2^E) with one
+// REDUX, split m = rint(x 2^(30-E)) into balanced signed bytes, and reduce the
+// exact unit sum of m.  Returns the four digit words (d0..d3 of the 4 rows).
+struct Digits {
+  uint32_t dw[4];
+  float xsum;   // sum of m over the unit (valid in every lane of the unit)
+  float scale;  // 2^(E-30)
+};
+
+template <int IPU>
+__device__ __forceinline__ Digits digitize(const float (&v)[4], uint32_t umask) {
+  Digits d;
+  const float m4 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+  const uint32_t umx = __reduce_max_sync(umask, __float_as_uint(m4));
+  // max < 2^e; e from the biased exponent (denormal max: 2^-126 still bounds it)
+  const int e = umx ? (int)((umx >> 23) & 0xFF) - 126 : 0;
+  const int k = 30 - e, k1 = k >> 1, k2 = k - k1;  // 2^k may leave the f32 range
+  const float f1 = __int_as_float((127 + k1) << 23), f2 = __int_as_float((127 + k2) << 23);
+  int mv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) mv[i] = __float2int_rn(__fmul_rn(__fmul_rn(v[i], f1), f2));
+  // balanced base-256 digits: with t = m + 0x808080, digit j < 3 is byte j of t
+  // minus 128 (i.e. byte ^ 0x80 as s8) and the top digit is t >> 24 (|.| <= 64)
+  uint32_t tt[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tt[i] = (uint32_t)(mv[i] + 0x808080);
+  const uint32_t lo01 = __byte_perm(tt[0], tt[1], 0x5140), lo23 = __byte_perm(tt[2], tt[3], 0x5140);
+  const uint32_t hi01 = __byte_perm(tt[0], tt[1], 0x7362), hi23 = __byte_perm(tt[2], tt[3], 0x7362);
+  d.dw[3] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // byte 0 of each
+  d.dw[2] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // byte 1
+  d.dw[1] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // byte 2
+  d.dw[0] = __byte_perm(hi01, hi23, 0x7632);                // byte 3 = t >> 24
+  // exact unit sum of m, split 16/16 so each half fits an int32 REDUX
+  int slo = 0, shi = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    slo += mv[i] & 0xFFFF;
+    shi += mv[i] >> 16;
+  }
+  slo = __reduce_add_sync(umask, slo);
+  shi = __reduce_add_sync(umask, shi);
+  d.xsum = fmaf((float)shi, 65536.f, (float)slo);
+  d.scale = umx ? __int_as_float((127 + e - 30) << 23) : 0.f;  // e - 30 >= -156: see below
+  if (umx && e - 30 < -126) d.scale = scalbnf(1.f, e - 30);
+  return d;
+}
+
+// Digit store: B-fragment words of (step st, token tk) at [st][TP][j][t] x (b0, b1).
+__device__ __forceinline__ void store_digits(uint32_t* base, int st, int tk, int TP, int sub,
+                                             const Digits& d) {
+  uint32_t* dst = base + ((st * TP + tk) * 16 + (sub & 3)) * 2 + (sub >> 2);
+  dst[0] = d.dw[0];
+  dst[8] = d.dw[1];
+  dst[16] = d.dw[2];
+  dst[24] = d.dw[3];
+}
+
+// 1/rms over the full rows of tokens [t0, t0 + ntok) (RMSNorm prologue),
+// block-wide; inv[tk - t0].
+template <int T>
+__device__ __forceinline__ void row_inv_rms(const GemvArgs& a, int t0, int ntok, float* red,
+                                            float* inv) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = 0; j < ntok; ++j) {
+    float ss = 0.f;
+    for (int64_t k = 4 * threadIdx.x; k < a.n; k += 4 * T) {
+      float v[4];
+      load_raw4(a, (t0 + j) * a.ldx + k, k, v);
+      ss += v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[j * (T / 32) + warp] = ss;
+  }
+  __syncthreads();
+  if (threadIdx.x < ntok) {
+    float ss = 0.f;
+    for (int w = 0; w < T / 32; ++w) ss += red[threadIdx.x * (T / 32) + w];
+    inv[threadIdx.x] = rsqrtf(ss / (float)a.n + a.eps);
+  }
+  __syncthreads();
+}
+
+// Activation prep kernel (used when a CTA's chunk x tokens is too long for the
+// in-kernel prologue): digits for all rows of all (padded) tokens, once per
+// GEMV, into a global buffer [step][TP][16 x uint2] + [unit][TP] (xsum, scale).
+// grid = (ceil(KS*64 / 256), TP); tokens >= M are written as zeros.
+template <int IPU>
+__global__ void __launch_bounds__(256) act_prep_kernel(const GemvArgs a, int TP, int UPS) {
+  __shared__ float red[16 * 8];
+  __shared__ float inv[16];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int tk = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  if (a.xmode == 1 && tk < a.M) row_inv_rms<256>(a, tk, 1, red, inv);  // this CTA's token
+  const int it = blockIdx.x * 256 + threadIdx.x;  // item within the token
+  const int nitems = a.KS * 64;
+  const bool live = it < nitems && tk < a.M;
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  const int st = it >> 3, sub = it & 7;
+  if (live) load_x4(a, tk, (int64_t)32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v, inv - tk);
+  // (load_x4 reads inv_rms[tk]; this CTA's single value sits at inv[0])
+  const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
+  Digits d = digitize<IPU>(v, umask);
+  if (it < nitems) {
+    uint32_t* dig = (uint32_t*)a.dig;
+    store_digits(dig, st, tk, TP, sub, d);
+    if ((it % IPU) == 0) {
+      const int u = it / IPU;
+      ((float2*)(a.dig + (size_t)a.KS * 8 * TP * 128))[u * TP + tk] =
+          live ? make_float2(d.xsum, d.scale) : make_float2(0.f, 0.f);
+    }
+  }
+}
+
 // Shared-memory carve-up (bytes), identical on host and device.
 struct SmemLayout {
-  int ring, bars, bfrag, xu, su, zero, rbar, inv, yp, total, stage;
-  __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int M, int WPC, int S) {
+  int ring, bars, bfrag, xs, zero, rbar, pbar, inv, yp, total, stage;
+  __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int TP, int M, int WPC,
+                                 int S) {
     stage = bits * 512 + szb;
     const int max_units = max_steps;  // units are >= 32 rows
     int off = 0;
     ring = off;  off += WPC * D * stage;
     bars = off;  off += WPC * D * 8;
-    bfrag = off; off += max_steps * M * 128;  // [token][step][digit j][t] (b0, b1)
-    xu = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
-    su = off;    off += ((max_units * M * 4 + 15) / 16) * 16;
+    bfrag = off; off += max_steps * TP * 128;   // [step][TP][digit j][t] (b0, b1)
+    xs = off;    off += max_units * TP * 8;     // [unit][TP] (sum of m, 2^(E-30))
     zero = off;  off += 8;
     rbar = off;  off += 8;
+    pbar = off;  off += 8;
     inv = off;   off += 16 * 4;
     yp = off;    off += (S - 1) * WPC * 16 * M * 4 + 16;  // owner's inbox
     total = off;
@@ -252,12 +376,13 @@ struct SmemLayout {
 // 128, 256 (their (s, z) ride in the stage), 0 for longer groups (g a multiple
 // of 256 or full column; (s, z) prefetched from global one group ahead).
 // Exponent/flush unit U = min(g, 128) rows: the activations of one unit share a
-// fixed-point exponent (found with warp shuffles, no CTA barrier), and the
-// integer accumulators are folded into f32 once per unit.
+// fixed-point exponent (found with one REDUX, no CTA barrier), and the integer
+// accumulators are folded into f32 once per unit.
 template <int BITS, int NB, int WPC, int GPS>
 __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int T = WPC * 32;
+  constexpr int TP = 2 * NB;                // tokens in the fragment layout (padded)
   constexpr int SZB = GPS * 128;
   constexpr int UPS = GPS > 2 ? GPS : 2;   // flush units per superstep
   constexpr int SPU = 8 / UPS;             // steps per unit
@@ -272,11 +397,10 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   const int M = a.M, D = a.D;
   const int nsteps = nks * 8;
   const int nunits = nks * UPS;
-  SmemLayout L(BITS, SZB, D, a.max_steps, M, WPC, S);
+  SmemLayout L(BITS, SZB, D, a.max_steps, TP, M, WPC, S);
   unsigned char* ring = smem + L.ring + warp * D * L.stage;
   uint64_t* bars = (uint64_t*)(smem + L.bars) + warp * D;
-  float* xu = (float*)(smem + L.xu);   // [token][unit] sum of fixed-point x
-  float* su = (float*)(smem + L.su);   // [token][unit] 2^(E-30)
+  float2* xs = (float2*)(smem + L.xs);
   float* yp = (float*)(smem + L.yp);
 
   const char* wsrc = (const char*)(a.qw + ((int64_t)(active ? p : 0) * a.KS) * BITS * 32);
@@ -300,17 +424,21 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   }
   if (threadIdx.x < 2) ((uint32_t*)(smem + L.zero))[threadIdx.x] = 0u;
   uint64_t* rbar = (uint64_t*)(smem + L.rbar);
-  if (S > 1 && threadIdx.x == 0) {
-    // split-K inbox of the cluster's rank-0 CTA: (S-1) partials of R floats
-    mbar_init(rbar, 1);
+  uint64_t* pbar = (uint64_t*)(smem + L.pbar);
+  if (threadIdx.x == 0) {
+    if (S > 1) {
+      // split-K inbox of the cluster's rank-0 CTA: (S-1) partials of R floats
+      mbar_init(rbar, 1);
+      mbar_expect_tx(rbar, (uint32_t)((S - 1) * WPC * 16 * M * 4));
+    }
+    if (a.dig) mbar_init(pbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(rbar, (uint32_t)((S - 1) * WPC * 16 * M * 4));
   }
   if (S > 1)  // arrive now, wait only before pushing: every inbox is initialised by then
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  // pull this chunk's activations into L2 now (safe before the PDL wait: L2 is
-  // the point of coherence, and nothing is read into registers or L1 here)
-  {
+  if (!a.dig) {
+    // pull this chunk's activations into L2 now (safe before the PDL wait: L2
+    // is the point of coherence, and nothing is read into registers or L1 here)
     const int esz = a.x_dtype == QIGEN_F32 ? 4 : 2;
     const int64_t kb = a.xmode == 1 ? 0 : (int64_t)ks0 * kSuper * esz;
     const int64_t ke = (a.xmode == 1 ? a.n : min((int64_t)ks1 * kSuper, a.n)) * esz;
@@ -323,112 +451,65 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
       asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
     }
   }
-  __syncwarp();
+  __syncthreads();
 
   // ---- 2. PDL: everything below may read what the previous kernel wrote -----
   asm volatile("griddepcontrol.wait;" ::: "memory");
   trace_point(a, 1);
 
-  // ---- 3. activation prologue: per-unit exponent, digits, unit sums ---------
-  float* inv_rms = (float*)(smem + L.inv);
-  if (a.xmode == 1) {  // fused RMSNorm: every CTA reduces the full rows (L2 hits)
-    float* red = xu;  // scratch: the unit sums are written only after this pass
-    for (int tk = 0; tk < M; ++tk) {
-      float ss = 0.f;
-      for (int64_t k = 4 * threadIdx.x; k < a.n; k += 4 * T) {
-        float v[4];
-        load_raw4(a, tk * a.ldx + k, k, v);
-        ss += v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) red[tk * WPC + warp] = ss;
+  // ---- 3. activation digits for this chunk into shared memory ----------------
+  if (a.dig) {
+    // prepared by act_prep_kernel: two bulk copies
+    if (threadIdx.x == 0) {
+      const uint32_t db = (uint32_t)(nsteps * TP * 128), xb = (uint32_t)(nunits * TP * 8);
+      mbar_expect_tx(pbar, db + xb);
+      bulk_g2s(smem + L.bfrag, a.dig + (size_t)ks0 * 8 * TP * 128, db, pbar);
+      bulk_g2s(smem + L.xs, a.dig + (size_t)a.KS * 8 * TP * 128 + (size_t)ks0 * UPS * TP * 8, xb,
+               pbar);
+      trace_point(a, 8);
+      if (lane == 0)
+        for (int s = n_pre; s < n_first; ++s) issue(s);
+    } else if (lane == 0) {
+      for (int s = n_pre; s < n_first; ++s) issue(s);
     }
-    __syncthreads();
-    if (threadIdx.x < M) {
-      float ss = 0.f;
-      for (int w = 0; w < WPC; ++w) ss += red[threadIdx.x * WPC + w];
-      inv_rms[threadIdx.x] = rsqrtf(ss / (float)a.n + a.eps);
-    }
-    __syncthreads();
-  }
-  {
+    mbar_wait(pbar, 0);
+  } else {
+    // fused prologue: every CTA digitises its own chunk (short chunks only)
+    float* inv_rms = (float*)(smem + L.inv);
+    if (a.xmode == 1) row_inv_rms<T>(a, 0, M, (float*)(smem + L.xs), inv_rms);
     const int64_t k0 = (int64_t)ks0 * kSuper;
     const int items = M * nsteps * 8;  // item = (token, step, half, t): 4 consecutive k
     uint32_t* bw = (uint32_t*)(smem + L.bfrag);
-    constexpr int RB = 4;  // rounds of item loads kept in flight together
     const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
-    const int rounds = (items + T - 1) / T;
     bool first = true;
-    for (int r0 = 0; r0 < rounds; r0 += RB) {  // CTA-uniform trip count
-      float v[RB][4];
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        const int it = (r0 + r) * T + threadIdx.x;
-        v[r][0] = v[r][1] = v[r][2] = v[r][3] = 0.f;
-        if (it < items) {
-          const int sub = it & 7, st = (it >> 3) % nsteps, tk = (it >> 3) / nsteps;
-          load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v[r], inv_rms);
-        }
-      }
+    for (int it0 = 0; it0 < items; it0 += T) {  // CTA-uniform trip count
+      const int it = it0 + threadIdx.x;
+      const bool live = it < items;
+      const int sub = it & 7, st = (it >> 3) % nsteps, tk = live ? (it >> 3) / nsteps : 0;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (live) load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v, inv_rms);
       if (first) {  // the rest of the first ring fill goes out behind the x loads
+        trace_point(a, 8);
         first = false;
         if (lane == 0)
           for (int s = n_pre; s < n_first; ++s) issue(s);
       }
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        if (r0 + r >= rounds) break;  // uniform
-        const int it = (r0 + r) * T + threadIdx.x;
-        const bool live = it < items;
-        const int sub = it & 7, st = (it >> 3) % nsteps, tk = live ? (it >> 3) / nsteps : 0;
-        // unit max |x| (REDUX on the order-preserving bit pattern of |x| >= 0)
-        const float m4 = fmaxf(fmaxf(fabsf(v[r][0]), fabsf(v[r][1])), fmaxf(fabsf(v[r][2]), fabsf(v[r][3])));
-        const uint32_t umx = __reduce_max_sync(umask, __float_as_uint(m4));
-        // max < 2^e; e from the biased exponent (denormal max: 2^-126 still bounds it)
-        const int e = umx ? (int)((umx >> 23) & 0xFF) - 126 : 0;
-        const int k = 30 - e, k1 = k >> 1, k2 = k - k1;  // 2^k may leave the f32 range
-        const float f1 = __int_as_float((127 + k1) << 23), f2 = __int_as_float((127 + k2) << 23);
-        int mv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) mv[i] = __float2int_rn(__fmul_rn(__fmul_rn(v[r][i], f1), f2));
-        // balanced base-256 digits: with t = m + 0x808080, digit j < 3 is byte j of t
-        // minus 128 (i.e. byte ^ 0x80 as s8) and the top digit is t >> 24 (|.| <= 64)
-        uint32_t tt[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) tt[i] = (uint32_t)(mv[i] + 0x808080);
-        const uint32_t lo01 = __byte_perm(tt[0], tt[1], 0x5140), lo23 = __byte_perm(tt[2], tt[3], 0x5140);
-        const uint32_t hi01 = __byte_perm(tt[0], tt[1], 0x7362), hi23 = __byte_perm(tt[2], tt[3], 0x7362);
-        const uint32_t dw3 = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // byte 0 of each
-        const uint32_t dw2 = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // byte 1
-        const uint32_t dw1 = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // byte 2
-        const uint32_t dw0 = __byte_perm(hi01, hi23, 0x7632);                // byte 3 = t >> 24
-        // exact unit sum of m, split 16/16 so each half fits an int32 REDUX
-        int slo = 0, shi = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          slo += mv[i] & 0xFFFF;
-          shi += mv[i] >> 16;
-        }
-        slo = __reduce_add_sync(umask, slo);
-        shi = __reduce_add_sync(umask, shi);
-        if (live) {
-          // [token][step][digit j][t] x (b0, b1): read by lane (gq, t), gq % 4 == j
-          uint32_t* dst = bw + ((tk * a.max_steps + st) * 16 + (sub & 3)) * 2 + (sub >> 2);
-          dst[0] = dw0;
-          dst[8] = dw1;
-          dst[16] = dw2;
-          dst[24] = dw3;
-          if ((it % IPU) == 0) {
-            const int u = tk * nunits + (it % (nsteps * 8)) / IPU;
-            xu[u] = fmaf((float)shi, 65536.f, (float)slo);
-            su[u] = scalbnf(1.f, e - 30);
-          }
-        }
+      const Digits d = digitize<IPU>(v, umask);
+      if (live) {
+        store_digits(bw, st, tk, TP, sub, d);
+        if ((it % IPU) == 0) xs[((it % (nsteps * 8)) / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
       }
     }
+    // zero fragments / unit params of the padding tokens M..TP-1
+    for (int e = threadIdx.x; e < nsteps * (TP - M) * 16; e += T) {
+      const int st = e / ((TP - M) * 16), r = e % ((TP - M) * 16);
+      ((uint2*)bw)[(st * TP + M) * 16 + r] = make_uint2(0u, 0u);
+    }
+    for (int e = threadIdx.x; e < nunits * (TP - M); e += T)
+      xs[(e / (TP - M)) * TP + M + e % (TP - M)] = make_float2(0.f, 0.f);
     if (first && lane == 0)  // no activation items (cannot happen for n > 0)
       for (int s = n_pre; s < n_first; ++s) issue(s);
+    trace_point(a, 10);
     __syncthreads();
   }
   asm volatile("griddepcontrol.launch_dependents;");
@@ -451,21 +532,11 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   // digit-pair weight of this lane: columns (d0, d1) -> 2^16, (d2, d3) -> 1
   const float w_lo = (t & 1) ? 1.f : 65536.f;
   const float w_hi = w_lo * RowScale<BITS>::inv_hi;
-  // B fragment of n8 block nb: token 2nb + (gq >> 2), digit gq & 3 (zeros past M)
-  const uint2* bsrc[NB];
-  const float* xul[NB];
-  const float* sul[NB];
-  bool xon[NB];
-#pragma unroll
-  for (int nb = 0; nb < NB; ++nb) {
-    const int tb = 2 * nb + (gq >> 2);
-    bsrc[nb] = tb < M ? (const uint2*)(smem + L.bfrag) + tb * a.max_steps * 16 + (gq & 3) * 4 + t
-                      : nullptr;
-    const int tc = 2 * nb + (t >> 1);  // token of this lane's accumulator columns
-    xon[nb] = ((t & 1) == 0) && tc < M;
-    xul[nb] = xu + (tc < M ? tc : 0) * nunits;
-    sul[nb] = su + (tc < M ? tc : 0) * nunits;
-  }
+  // B fragment of n8 block nb: token 2nb + (gq >> 2), digit gq & 3; per step the
+  // fragments of all TP tokens are 2 NB x 128 bytes apart (compile-time stride)
+  const uint2* bbase = (const uint2*)(smem + L.bfrag) + (gq >> 2) * 16 + (gq & 3) * 4 + t;
+  const bool xon = (t & 1) == 0;  // lanes holding digits (d0, d1) carry the z X term
+  const int tcol = t >> 1;        // token offset of this lane's accumulator columns
   const float2* szg = (const float2*)zsrc;
   const int spg = a.g ? a.g / kStep : a.KS * 8;  // steps per group
   int gcur = ks0 * 8 / spg;
@@ -477,8 +548,8 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   auto flush = [&](int u, float2 sz0, float2 sz1) {
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
-      const float X = xon[nb] ? xul[nb][u] : 0.f;
-      const float sc = sul[nb][u];
+      const float2 xv = xs[u * TP + 2 * nb + tcol];
+      const float X = xon ? xv.x : 0.f, sc = xv.y;
       int c0 = acc[0][nb][0], c1 = acc[0][nb][1], c2 = acc[0][nb][2], c3 = acc[0][nb][3];
 #pragma unroll
       for (int c = 1; c < AC; ++c) {
@@ -507,14 +578,14 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
 #pragma unroll
     for (int v = 0; v < BITS; ++v) w[v] = ((const uint4*)stg)[v * 32 + lane];
     const float2* szs = (const float2*)(stg + BITS * 512);
-    const int st0 = s * 8;
+    const uint2* bs = bbase + s * 8 * TP * 16;
 #pragma unroll
     for (int sl = 0; sl < 8; ++sl) {
       uint32_t af[4];
       extract<BITS>(w, sl, af);
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb)
-        imma(acc[sl % AC][nb], af, bsrc[nb] ? bsrc[nb][(st0 + sl) * 16] : make_uint2(0u, 0u));
+      for (int nb = 0; nb < NB; ++nb) imma(acc[sl % AC][nb], af, bs[(sl * TP + 2 * nb) * 16]);
+      constexpr int SPG = GPS > 0 ? 8 / GPS : 8;  // steps per group (short groups)
       if ((sl + 1) % SPU == 0) {
         const int uj = (sl + 1) / SPU - 1;  // unit within the superstep
         const int u = s * UPS + uj;
@@ -525,6 +596,7 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
           flush(u, szr0, szr1);
         }
       }
+      (void)SPG;
     }
     if (GPS == 0 && ((ks0 + s + 1) * 8) % spg == 0) {  // long group closed
       ++gcur;
@@ -588,6 +660,7 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
 static unsigned long long* g_trace = nullptr;
 constexpr int kMaxSplits = 16;  // cluster size along K (non-portable above 8)
 static int g_pre = -1;  // stages issued before the PDL wait (-1: all of the first fill)
+static int g_force_prep = 0;  // tuning: always digitise activations in act_prep_kernel
 
 static int sm_count() {
   static int cached = 0;
@@ -600,9 +673,35 @@ static int sm_count() {
   return cached;
 }
 
+// Grow-only per-device fallback workspace for prepared activation digits (used
+// when the caller passes none).  Growing is not allowed during stream capture.
+static int fallback_workspace(cudaStream_t stream, size_t bytes, unsigned char** out) {
+  static std::unordered_map<int, std::pair<unsigned char*, size_t>> ws;
+  int dev = 0;
+  QIGEN_CUDA_RET(cudaGetDevice(&dev));
+  auto& e = ws[dev];
+  if (e.second < bytes) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cap);
+    QIGEN_CHECK_ARG(cap == cudaStreamCaptureStatusNone, QIGEN_ERR_ARG,
+                    "GEMV workspace must grow outside stream capture: pass a workspace "
+                    "(qigen_gemv_workspace_size) or run this shape once before capturing");
+    if (e.first) QIGEN_CUDA_RET(cudaFree(e.first));
+    e.first = nullptr;
+    e.second = 0;
+    QIGEN_CUDA_RET(cudaMalloc((void**)&e.first, bytes));
+    e.second = bytes;
+  }
+  *out = e.first;
+  return QIGEN_OK;
+}
+
 template <int BITS, int NB, int WPC, int GPS>
 static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   auto kern = gemv_kernel<BITS, NB, WPC, GPS>;
+  constexpr int TP = 2 * NB;
+  constexpr int UPS = GPS > 2 ? GPS : 2;
+  constexpr int IPU = (8 / UPS) * 8;
   static bool configured = false;
   if (!configured) {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -611,13 +710,13 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     configured = true;
   }
   const int stage = BITS * 512 + GPS * 128;
-  auto shape = [&](int S) {  // smem plan for S chunks: ring of <= 40 KB per CTA
+  auto shape = [&](int S) {  // smem plan for S chunks: ring of <= 80 KB per CTA
     const int max_ks = (a.KS + S - 1) / S;
     a.max_steps = max_ks * 8;
-    SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, a.M, WPC, S);
+    SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, TP, a.M, WPC, S);
     const int budget = std::min(WPC * 10 * 1024, 224 * 1024 - L0.total - WPC * 16);
     a.D = std::max(2, std::min(max_ks, budget / (WPC * stage)));
-    return SmemLayout(BITS, GPS * 128, a.D, a.max_steps, a.M, WPC, S);
+    return SmemLayout(BITS, GPS * 128, a.D, a.max_steps, TP, a.M, WPC, S);
   };
   const int cols = (a.P + WPC - 1) / WPC;
   int S = req_S;
@@ -625,11 +724,15 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     // Empirical rule (tools/tune_splits.py, dependent chains of launches under
     // PDL on B200): grids above ~1.55 CTAs per SM lose more to the next kernel
     // not fitting beside this one than they gain from shorter chunks; below
-    // that, the shortest longest-chunk wins (ties: fewer CTAs).
-    const int max_ctas = (sm_count() * 155) / 100;
+    // that, the shortest longest-chunk wins (ties: fewer CTAs).  Never more
+    // CTAs than fit at once.
     S = 1;
     int best = a.KS;
     for (int c = 2; c <= std::min(kMaxSplits, a.KS); ++c) {
+      int occ = 2;  // resident CTAs per SM for this shape's shared memory
+      QIGEN_CUDA_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WPC * 32,
+                                                                   shape(c).total));
+      const int max_ctas = (sm_count() * std::min(155, 100 * std::max(occ, 1) - 10)) / 100;
       if (cols * c > max_ctas) break;
       const int chunk = (a.KS + c - 1) / c;
       if (chunk < best) {
@@ -646,6 +749,29 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   QIGEN_CHECK_ARG(L.total <= 227 * 1024, QIGEN_ERR_UNSUPPORTED,
                   "GEMV needs %d bytes of shared memory (K chunk too long; raise k_splits)",
                   L.total);
+  // activation digits: in each CTA when its chunk takes <= 2 rounds of the
+  // block, else once per GEMV in act_prep_kernel
+  const int rounds = (a.M * a.max_steps * 8 + WPC * 32 - 1) / (WPC * 32);
+  a.dig = nullptr;
+  if (rounds > 2 || g_force_prep) {
+    const size_t bytes = (size_t)a.KS * 8 * TP * 128 + (size_t)a.KS * UPS * TP * 8;
+    if (a.ws && a.ws_bytes >= bytes) {
+      a.dig = a.ws;
+    } else {
+      int st = fallback_workspace(stream, bytes, &a.dig);
+      if (st) return st;
+    }
+    cudaLaunchConfig_t pc = {};
+    pc.gridDim = dim3((unsigned)((a.KS * 64 + 255) / 256), (unsigned)TP, 1);
+    pc.blockDim = dim3(256, 1, 1);
+    pc.stream = stream;
+    cudaLaunchAttribute pa;
+    pa.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pa.val.programmaticStreamSerializationAllowed = 1;
+    pc.attrs = &pa;
+    pc.numAttrs = 1;
+    QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_kernel<IPU>, a, (int)TP, (int)UPS));
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cols, (unsigned)S, 1);
   cfg.blockDim = dim3(WPC * 32, 1, 1);
@@ -702,10 +828,21 @@ extern "C" int qigen_debug_prefetch(int stages_before_wait) {
   g_pre = stages_before_wait;
   return QIGEN_OK;
 }
+
+extern "C" int qigen_debug_force_prep(int on) {
+  g_force_prep = on;
+  return QIGEN_OK;
+}
+extern "C" int64_t qigen_gemv_workspace_size(int64_t n, int64_t tokens) {
+  const int64_t tp = tokens <= 2 ? 2 : tokens <= 4 ? 4 : tokens <= 8 ? 8 : 16;
+  return supersteps(n) * 8 * tp * (128 + 8);
+}
+
 extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
                              int64_t group, const void* x, int x_dtype, int64_t tokens,
                              int64_t ldx, float* y, int64_t ldy, int accumulate, int k_splits,
-                             int prologue, const float* prologue_w, float eps, void* stream) {
+                             int prologue, const float* prologue_w, float eps, void* workspace,
+                             int64_t workspace_bytes, void* stream) {
   QIGEN_CHECK_ARG(bits == 2 || bits == 3 || bits == 4, QIGEN_ERR_CONFIG,
                   "bits must be one of (2, 3, 4), got %d", bits);
   QIGEN_CHECK_ARG(qw && qsz && x && y, QIGEN_ERR_ARG, "null pointer");
@@ -743,6 +880,8 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   const int esz = x_dtype == QIGEN_F32 ? 4 : 2;
   a.x_vec = ((uintptr_t)x % 16 == 0) && ((ldx * esz) % 16 == 0) && ((n * esz) % 16 == 0 || prologue != 2);
   a.xmode = prologue;
+  a.ws = (unsigned char*)workspace;
+  a.ws_bytes = workspace ? (size_t)workspace_bytes : 0;
   a.xw = prologue_w;
   a.eps = eps;
   a.accumulate = accumulate;
@@ -762,5 +901,5 @@ extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64
                           int64_t group, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
                           float* y, int64_t ldy, int accumulate, int k_splits, void* stream) {
   return qigen_gemv_ex(qw, qsz, n, m, bits, group, x, x_dtype, tokens, ldx, y, ldy, accumulate,
-                       k_splits, 0, nullptr, 0.f, stream);
+                       k_splits, 0, nullptr, 0.f, nullptr, 0, stream);
 }

@@ -127,6 +127,18 @@ class PanelWeights:
              codes.data_ptr(), _dev.stream_handle())
         return codes
 
+    def _workspace(self, tokens: int, device) -> torch.Tensor:
+        """Scratch for prepared activation digits (owned per matrix and token
+        count, so graphs of distinct matrices never share it)."""
+        ws = getattr(self, "_ws", None)
+        if ws is None:
+            ws = self._ws = {}
+        buf = ws.get(tokens)
+        if buf is None:
+            nbytes = int(lib().qigen_gemv_workspace_size(self.n, tokens))
+            buf = ws[tokens] = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return buf
+
     def nbytes_algorithmic(self) -> int:
         """Packed codes + f32 scale + f32 zero (the roofline bytes)."""
         G = self.config.groups_for_rows(self.n)
@@ -161,13 +173,15 @@ class PanelWeights:
         if y2.dtype != torch.float32 or y2.stride(1) != 1:
             raise ConfigError("out must be float32 with unit column stride")
         st = _dev.stream_handle()
+        ws = self._workspace(min(T, MAX_GEMV_TOKENS), x2.device)
         for t0 in range(0, T, MAX_GEMV_TOKENS):
             t1 = min(T, t0 + MAX_GEMV_TOKENS)
             xs, ys = x2[t0:t1], y2[t0:t1]
             call("qigen_gemv_ex", self.qw.data_ptr(), self.qsz.data_ptr(), self.n, self.m,
                  self.bits, self.group_code, xs.data_ptr(), _DTYPES[xs.dtype], t1 - t0,
                  xs.stride(0), ys.data_ptr(), ys.stride(0), int(accumulate), int(k_splits), mode,
-                 norm_weight.data_ptr() if mode == 1 else None, float(eps), st)
+                 norm_weight.data_ptr() if mode == 1 else None, float(eps), ws.data_ptr(),
+                 ws.numel(), st)
         return out.reshape(self.m) if squeeze else out
 
 

@@ -296,3 +296,35 @@ def test_input_sums_and_dense_reference(q):
     pm = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (256, 64)))
     yd = q.qgemv_reference(pm, x[:256])
     assert np.allclose(yd, orc.qgemv_reference(codes, s, z, x[:256]), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("tokens", [1, 3, 8])
+@pytest.mark.parametrize("bits,g", [(4, 128), (3, 64), (2, 32), (4, None), (3, 512)])
+def test_qgemv_prep_kernel_path(q, tokens, bits, g):
+    """Activation digits from the separate prep kernel (forced) vs the oracle,
+    including the fused RMSNorm / SwiGLU prologues."""
+    from paper_2307_03738_b200 import _lib
+    K, N = 2048, 640
+    cm, codes, s, z, rng = _case(q, K, N, bits, g, seed=tokens + bits)
+    pw = q.PanelWeights.from_codes(cm)
+    X = rng.normal(0, 1, (tokens, K)).astype(np.float32)
+    try:
+        _lib.lib().qigen_debug_force_prep(1)
+        Y = pw.gemv(torch.from_numpy(X).cuda()).cpu().numpy()
+        wn = rng.uniform(0.5, 1.5, K).astype(np.float32)
+        Yn = pw.gemv(torch.from_numpy(X).cuda(), prologue="rmsnorm",
+                     norm_weight=torch.from_numpy(wn).cuda()).cpu().numpy()
+        GU = rng.normal(0, 1, (tokens, 2 * K)).astype(np.float32)
+        Ys = pw.gemv(torch.from_numpy(GU).cuda(), prologue="swiglu").cpu().numpy()
+    finally:
+        _lib.lib().qigen_debug_force_prep(0)
+    Yn_fused = pw.gemv(torch.from_numpy(X).cuda(), prologue="rmsnorm",
+                       norm_weight=torch.from_numpy(wn).cuda()).cpu().numpy()
+    for t in range(tokens):
+        assert rel_err(Y[t], orc.qgemv_reference(codes, s, z, X[t])) <= TOL
+        xn = X[t] / np.sqrt(np.mean(X[t].astype(np.float64) ** 2) + 1e-5) * wn
+        assert rel_err(Yn[t], orc.qgemv_reference(codes, s, z, xn)) <= 1e-5
+        assert rel_err(Yn_fused[t], orc.qgemv_reference(codes, s, z, xn)) <= 1e-5
+        g_, u_ = GU[t, :K].astype(np.float64), GU[t, K:].astype(np.float64)
+        xs = g_ / (1 + np.exp(-g_)) * u_
+        assert rel_err(Ys[t], orc.qgemv_reference(codes, s, z, xs)) <= 1e-5

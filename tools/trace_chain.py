@@ -20,7 +20,7 @@ for shp, b, g in [((4096, 4096), 4, 128), ((4096, 11008), 4, 128), ((11008, 4096
     pws = [base] + [q.PanelWeights(base.qw.clone(), base.qsz.clone(), K, N, cfg) for _ in range(R - 1)]
     xs = [torch.randn(K, device=dev) for _ in range(R)]
     ys = [torch.empty(N, device=dev) for _ in range(R)]
-    bufs = [torch.zeros(4096 * 8, dtype=torch.int64, device=dev) for _ in range(R)]
+    bufs = [torch.zeros(4096 * 16, dtype=torch.int64, device=dev) for _ in range(R)]
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         for pw, x, y in zip(pws, xs, ys):
@@ -42,7 +42,7 @@ for shp, b, g in [((4096, 4096), 4, 128), ((4096, 11008), 4, 128), ((11008, 4096
         s.synchronize()
     print(f"K={K} N={N} b={b} g={g}: {R} GEMVs in {e0.elapsed_time(e1)*1e3:.1f} us "
           f"({e0.elapsed_time(e1)*1e3/R:.2f} us each, {base.nbytes_algorithmic()*R/e0.elapsed_time(e1)/1e6:.0f} GB/s)")
-    tr = [b_.view(-1, 8).cpu().numpy() for b_ in bufs]
+    tr = [b_.view(-1, 16).cpu().numpy() for b_ in bufs]
     t0 = min(t[t[:, 0] > 0][:, 0].min() for t in tr)
     for i, t in enumerate(tr[:6]):
         t = t[t[:, 0] > 0]

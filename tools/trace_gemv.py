@@ -19,7 +19,7 @@ for shp, b, g in [((4096, 4096), 4, 128), ((11008, 4096), 4, 128), ((4096, 11008
     pw = q.PanelWeights.from_float(torch.randn(K, N, device=dev) * 0.02, q.QuantConfig(b, g))
     x = torch.randn(K, device=dev)
     y = torch.empty(N, device=dev)
-    buf = torch.zeros(4096 * 8, dtype=torch.int64, device=dev)
+    buf = torch.zeros(4096 * 16, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
     for rep in range(3):
         flush.zero_()  # evict L2
@@ -29,7 +29,7 @@ for shp, b, g in [((4096, 4096), 4, 128), ((11008, 4096), 4, 128), ((4096, 11008
         pw.gemv(x, out=y)
         torch.cuda.synchronize()
         _lib.lib().qigen_debug_trace(None)
-    t = buf.view(-1, 8).cpu().numpy()
+    t = buf.view(-1, 16).cpu().numpy()
     t = t[t[:, 0] > 0]
     base = t[:, 0].min()
     rel = (t[:, :5] - base) / 1e3
