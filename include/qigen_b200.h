@@ -134,6 +134,17 @@ int qigen_rope_kv(const float* qkv, int64_t batch, int64_t heads, int64_t head_d
 int qigen_rmsnorm_f16(const float* h, const float* w, int64_t rows, int64_t d, float eps,
                       void* out, void* stream);
 
+/* Small-batch quantized GEMM on the tcgen05 tensor cores (north_star (c)):
+ * weights dequantized to fp16 (w = s (c - z)) in shared memory, activations
+ * converted to fp16, f32 accumulation in TMEM.  4-bit, group 32..256 (dividing
+ * 256), 1..256 tokens (meant for tokens >= 16).  workspace >=
+ * qigen_gemm_tc_workspace_size bytes (the fp16 activation tiles). */
+int64_t qigen_gemm_tc_workspace_size(int64_t n, int64_t tokens);
+int qigen_gemm_tc(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+                  int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
+                  float* y, int64_t ldy, int accumulate, int k_splits, void* workspace,
+                  int64_t workspace_bytes, void* stream);
+
 /* Debugging aid: when buf is non-NULL every later qigen_gemv launch writes
  * %globaltimer stamps (entry, after the PDL wait, after the activation
  * prologue, after the main loop, exit, ...) to buf[(cta_y*grid_x + cta_x)*16 + i]. */

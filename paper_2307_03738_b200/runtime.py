@@ -30,6 +30,9 @@ from .quant import CodeMatrix, quantize_matrix
 
 _DTYPES = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
 MAX_GEMV_TOKENS = 16
+TC_MIN_TOKENS = 16   # north_star (c): tensor cores only from 16 tokens up
+MAX_TC_TOKENS = 256
+TC_ENABLED = [True]  # tests flip this to compare against the GEMV path
 
 
 @dataclass
@@ -127,17 +130,24 @@ class PanelWeights:
              codes.data_ptr(), _dev.stream_handle())
         return codes
 
-    def _workspace(self, tokens: int, device) -> torch.Tensor:
-        """Scratch for prepared activation digits (owned per matrix and token
-        count, so graphs of distinct matrices never share it)."""
+    def _workspace(self, key, device) -> torch.Tensor:
+        """Scratch for prepared activations (owned per matrix and token count,
+        so graphs of distinct matrices never share it)."""
         ws = getattr(self, "_ws", None)
         if ws is None:
             ws = self._ws = {}
-        buf = ws.get(tokens)
+        buf = ws.get(key)
         if buf is None:
-            nbytes = int(lib().qigen_gemv_workspace_size(self.n, tokens))
-            buf = ws[tokens] = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            if isinstance(key, tuple):
+                nbytes = int(lib().qigen_gemm_tc_workspace_size(self.n, key[1]))
+            else:
+                nbytes = int(lib().qigen_gemv_workspace_size(self.n, key))
+            buf = ws[key] = torch.empty(nbytes, dtype=torch.uint8, device=device)
         return buf
+
+    def _tc_ok(self) -> bool:
+        g = self.config.group_size
+        return self.bits == 4 and g in (32, 64, 128, 256) and TC_ENABLED[0]
 
     def nbytes_algorithmic(self) -> int:
         """Packed codes + f32 scale + f32 zero (the roofline bytes)."""
@@ -173,6 +183,17 @@ class PanelWeights:
         if y2.dtype != torch.float32 or y2.stride(1) != 1:
             raise ConfigError("out must be float32 with unit column stride")
         st = _dev.stream_handle()
+        if T >= TC_MIN_TOKENS and mode == 0 and self._tc_ok():
+            # small-batch GEMM on the tcgen05 tensor cores (north_star (c))
+            for t0 in range(0, T, MAX_TC_TOKENS):
+                t1 = min(T, t0 + MAX_TC_TOKENS)
+                xs, ys = x2[t0:t1], y2[t0:t1]
+                ws = self._workspace(("tc", t1 - t0), x2.device)
+                call("qigen_gemm_tc", self.qw.data_ptr(), self.qsz.data_ptr(), self.n, self.m,
+                     self.bits, self.group_code, xs.data_ptr(), _DTYPES[xs.dtype], t1 - t0,
+                     xs.stride(0), ys.data_ptr(), ys.stride(0), int(accumulate), int(k_splits),
+                     ws.data_ptr(), ws.numel(), st)
+            return out.reshape(self.m) if squeeze else out
         ws = self._workspace(min(T, MAX_GEMV_TOKENS), x2.device)
         for t0 in range(0, T, MAX_GEMV_TOKENS):
             t1 = min(T, t0 + MAX_GEMV_TOKENS)

@@ -198,7 +198,12 @@ def test_qgemv_small_batch(q, tokens):
     cm, codes, s, z, rng = _case(q, K, N, 4, 64, seed=tokens)
     pw = q.PanelWeights.from_codes(cm)
     X = rng.normal(0, 1, (tokens, K)).astype(np.float32)
-    Y = pw.gemv(torch.from_numpy(X).cuda()).cpu().numpy()
+    from paper_2307_03738_b200 import runtime as R
+    R.TC_ENABLED[0] = False  # the exact IMMA path at every token count
+    try:
+        Y = pw.gemv(torch.from_numpy(X).cuda()).cpu().numpy()
+    finally:
+        R.TC_ENABLED[0] = True
     for t in range(tokens):
         yref = orc.qgemv_reference(codes, s, z, X[t])
         assert rel_err(Y[t], yref) <= TOL, (tokens, t)
@@ -328,3 +333,49 @@ def test_qgemv_prep_kernel_path(q, tokens, bits, g):
         g_, u_ = GU[t, :K].astype(np.float64), GU[t, K:].astype(np.float64)
         xs = g_ / (1 + np.exp(-g_)) * u_
         assert rel_err(Ys[t], orc.qgemv_reference(codes, s, z, xs)) <= 1e-5
+
+
+TOL_TC = 2e-3  # tensor-core path: fp16 dequantized weights x fp16 activations, f32 accumulate
+
+
+@pytest.mark.parametrize("tokens", [16, 17, 33, 64, 100])
+@pytest.mark.parametrize("g", [32, 64, 128, 256])
+def test_small_batch_tensor_core_path(q, tokens, g):
+    """BASELINE configs[2] path (M >= 16): tcgen05 kernel vs the fp64 dense
+    oracle (and vs the exact IMMA path), ragged N and token counts."""
+    from paper_2307_03738_b200 import runtime as R
+    K, N = 2048, 1040
+    cm, codes, s, z, rng = _case(q, K, N, 4, g, seed=tokens + g)
+    pw = q.PanelWeights.from_codes(cm)
+    X = rng.normal(0, 1, (tokens, K)).astype(np.float32)
+    xt = torch.from_numpy(X).cuda()
+    Y = pw.gemv(xt).cpu().numpy()
+    ref = np.stack([orc.qgemv_reference(codes, s, z, X[t]) for t in range(tokens)])
+    assert rel_err(Y, ref) <= TOL_TC
+    R.TC_ENABLED[0] = False
+    try:
+        Y2 = pw.gemv(xt).cpu().numpy()
+    finally:
+        R.TC_ENABLED[0] = True
+    assert rel_err(Y2, ref) <= TOL
+    # accumulate into y and fp16 activations
+    Yacc = torch.from_numpy(Y).cuda()
+    pw.gemv(xt, out=Yacc, accumulate=True)
+    assert rel_err(Yacc.cpu().numpy(), 2 * ref) <= TOL_TC
+    Yh = pw.gemv(xt.half()).cpu().numpy()
+    refh = np.stack([orc.qgemv_reference(codes, s, z, X[t].astype(np.float16).astype(np.float32))
+                     for t in range(tokens)])
+    assert rel_err(Yh, refh) <= TOL_TC
+
+
+def test_cfg2_shapes_tensor_core(q):
+    """configs[2]: K = N = 8192, 4-bit g64, M in {16, 64}."""
+    K = N = 8192
+    cm, codes, s, z, rng = _case(q, K, N, 4, 64, seed=99)
+    pw = q.PanelWeights.from_codes(cm)
+    wd = q.dequantize_matrix(cm).double()
+    for M in (16, 64):
+        X = torch.from_numpy(rng.normal(0, 1, (M, K)).astype(np.float32)).cuda()
+        Y = pw.gemv(X).double()
+        ref = X.double() @ wd
+        assert ((Y - ref).abs().max() / (1 + ref.abs().max())).item() <= TOL_TC
