@@ -154,6 +154,8 @@ int qigen_debug_trace(void* buf);
 int qigen_debug_prefetch(int stages_before_wait);
 /* Tuning aid: 1 = always digitise activations in the separate prep kernel. */
 int qigen_debug_force_prep(int on);
+/* Tuning aid for the tensor-core path: 1 = skip A-tile stores, 2 = skip MMAs. */
+int qigen_debug_tc_mode(int mode);
 
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
 

@@ -59,6 +59,7 @@ SIGNATURES = {
     "qigen_debug_trace": (_I32, [_P]),
     "qigen_debug_prefetch": (_I32, [_I32]),
     "qigen_debug_force_prep": (_I32, [_I32]),
+    "qigen_debug_tc_mode": (_I32, [_I32]),
     "qigen_weights_create": (_I32, [_P, _I32, _I64, _I64, _I32, _I64, _I64, _I64, _P, _I64,
                                     _P, _P, _P, ctypes.POINTER(_P)]),
     "qigen_weights_destroy": (_I32, [_P]),

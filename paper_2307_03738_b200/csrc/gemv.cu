@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
 }
 
 // ---------------------------------------------------------------------------
-static unsigned long long* g_trace = nullptr;
+unsigned long long* g_trace = nullptr;  // shared with gemm_tc.cu
 constexpr int kMaxSplits = 16;  // cluster size along K (non-portable above 8)
 static int g_pre = -1;  // stages issued before the PDL wait (-1: all of the first fill)
 static int g_force_prep = 0;  // tuning: always digitise activations in act_prep_kernel
