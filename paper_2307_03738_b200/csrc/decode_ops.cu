@@ -37,11 +37,24 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, int B, int H, int 
 }
 
 // out[b] = f16(h[b] * rsqrt(mean(h[b]^2) + eps) * w); one CTA per row.
-__global__ void rmsnorm_f16_kernel(const float* __restrict__ h, const float* __restrict__ w, int d,
-                                   float eps, __half* __restrict__ out) {
+__global__ void __launch_bounds__(1024) rmsnorm_f16_kernel(const float* __restrict__ h,
+                                                          const float* __restrict__ w, int d,
+                                                          float eps, __half* __restrict__ out) {
+  // one CTA per row; 4 independent loads in flight per thread (a row of d <= 16K
+  // floats is one L2 round trip, not d / blockDim dependent ones)
+  constexpr int U = 4;
   const float* row = h + (size_t)blockIdx.x * d;
   float ss = 0.f;
-  for (int k = threadIdx.x; k < d; k += blockDim.x) ss += row[k] * row[k];
+  for (int k0 = threadIdx.x; k0 < d; k0 += blockDim.x * U) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * blockDim.x;
+      v[u] = k < d ? row[k] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) ss += v[u] * v[u];
+  }
   __shared__ float red[32];
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -80,7 +93,7 @@ extern "C" int qigen_rope_kv(const float* qkv, int64_t batch, int64_t heads, int
 extern "C" int qigen_rmsnorm_f16(const float* h, const float* w, int64_t rows, int64_t d,
                                  float eps, void* out, void* stream) {
   QIGEN_CHECK_ARG(h && w && out && rows > 0 && d > 0, QIGEN_ERR_ARG, "bad arguments");
-  rmsnorm_f16_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(h, w, (int)d, eps,
+  rmsnorm_f16_kernel<<<(unsigned)rows, 1024, 0, (cudaStream_t)stream>>>(h, w, (int)d, eps,
                                                                        (__half*)out);
   QIGEN_CUDA_RET(cudaGetLastError());
   return QIGEN_OK;

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(64, 1) stream(const char* src, int64_t per_cta
 
 
 // NW independent producer/consumer warp pairs per CTA (ring of D stages of B bytes each)
+template <int LANE0>
 __global__ void __launch_bounds__(1024, 1) multi(const char* src, int64_t per_cta, int B, int D, int NW,
                                                  unsigned* sink) {
   extern __shared__ __align__(128) unsigned char sm[];
@@ -93,6 +94,14 @@ __global__ void __launch_bounds__(1024, 1) multi(const char* src, int64_t per_ct
   if ((warp & 1) == 0) {
     for (int s = 0; s < nst; ++s) {
       const int slot = pair * D + s % D;
+      if (LANE0) {
+        if ((threadIdx.x & 31) == 0) {
+          if (s >= D) wait(&empty[slot], ((s / D) - 1) & 1);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&full[slot])), "r"(B) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(saddr(sm + (size_t)slot * B)), "l"(base + (int64_t)s * B), "r"(B), "r"(saddr(&full[slot])) : "memory");
+        }
+      } else {
       if (s >= D) wait(&empty[slot], ((s / D) - 1) & 1);
       if (elect()) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&full[slot])), "r"(B) : "memory");
@@ -100,6 +109,7 @@ __global__ void __launch_bounds__(1024, 1) multi(const char* src, int64_t per_ct
                      ::"r"(saddr(sm + (size_t)slot * B)), "l"(base + (int64_t)s * B), "r"(B), "r"(saddr(&full[slot])) : "memory");
       }
       __syncwarp();
+      }
     }
   } else {
     unsigned acc = 0;
@@ -142,19 +152,22 @@ int main() {
   struct Cfg { int B, D, NP; } cfgs[] = {
       {2560, 4, 8}, {2560, 6, 8}, {2560, 10, 8}, {2048, 6, 8}, {4096, 6, 8}, {8192, 4, 4},
       {8192, 8, 2}, {16384, 6, 1}, {32768, 4, 1}, {32768, 6, 1}, {2048, 32, 1}, {2048, 64, 1}};
-  cudaFuncSetAttribute(multi, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(multi<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(multi<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   struct M { int B, D, NW; } ms_[] = {{2048, 6, 1}, {2048, 6, 4}, {2048, 6, 8}, {2048, 6, 16}, {4096, 4, 8}, {8192, 3, 8}};
+  for (int l0 = 0; l0 < 2; ++l0)
   for (auto c : ms_) {
     const int64_t per_cta = (total / sms) / ((int64_t)c.B * c.NW) * ((int64_t)c.B * c.NW);
     const size_t smem = (size_t)c.NW * c.D * c.B + 2 * c.NW * c.D * 8;
     float best = 1e9;
     for (int r = 0; r < 3; ++r) {
       cudaEventRecord(e0);
-      multi<<<sms, 64 * c.NW, smem>>>(src, per_cta, c.B, c.D, c.NW, sink);
+      if (l0) multi<1><<<sms, 64 * c.NW, smem>>>(src, per_cta, c.B, c.D, c.NW, sink);
+      else multi<0><<<sms, 64 * c.NW, smem>>>(src, per_cta, c.B, c.D, c.NW, sink);
       cudaEventRecord(e1); cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
     }
-    printf("multi B=%6d D=%d NW=%2d: %7.1f GB/s err=%s\n", c.B, c.D, c.NW, (double)(per_cta / c.NW / c.B * c.B * c.NW) * sms / best / 1e6,
+    printf("multi %s B=%6d D=%d NW=%2d: %7.1f GB/s err=%s\n", l0 ? "lane0" : "elect", c.B, c.D, c.NW, (double)(per_cta / c.NW / c.B * c.B * c.NW) * sms / best / 1e6,
            cudaGetErrorString(cudaGetLastError()));
   }
   for (int u : {4, 8}) {
@@ -168,7 +181,7 @@ int main() {
     }
     printf("ldg U=%d: %7.1f GB/s\n", u, (double)total / best / 1e6);
   }
-  for (int spin_ = 0; spin_ < 1; ++spin_)
+  for (int spin_ = 0; spin_ < 0; ++spin_)
   for (auto c : cfgs) {
     const int64_t per_cta = (total / sms) / ((int64_t)c.B * c.NP) * ((int64_t)c.B * c.NP);
     const size_t smem = (size_t)c.NP * c.D * c.B + 2 * c.NP * c.D * 8;
