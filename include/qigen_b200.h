@@ -41,6 +41,15 @@ typedef enum { QIGEN_ZERO_REAL32 = 0, QIGEN_ZERO_QUANTIZED = 1 } qigen_zero_mode
 typedef enum { QIGEN_LAYOUT_ROW_SEQUENTIAL = 0, QIGEN_LAYOUT_ZCURVE = 1 } qigen_layout; /* packing.py:30-32 */
 typedef enum { QIGEN_F32 = 0, QIGEN_F16 = 1, QIGEN_BF16 = 2 } qigen_dtype;
 
+/* Flags for the `accumulate` argument of the GEMV entry points (bit set). */
+#define QIGEN_GEMV_ACCUMULATE 1 /* y += x W instead of y = x W */
+/* x is not written by the kernel launched just before this one on the stream
+ * (e.g. independent GEMVs back to back): the GEMV reads and digitises x before
+ * its programmatic-dependent-launch wait and waits only before writing y, so it
+ * overlaps its predecessor completely.  Never set it when x is the previous
+ * kernel's output. */
+#define QIGEN_GEMV_X_READY 2
+
 int qigen_version(void);
 const char* qigen_last_error(void);
 
@@ -101,7 +110,8 @@ int qigen_input_sums(const float* x, int64_t n, int64_t group_size, float* out, 
 /* Replaces qgemv(pm, x, sums, threads) and the generated
  * kernel it drives (kernelgen.py:371-423).  x: `tokens` rows of n activations
  * (dtype x_dtype, row stride ldx elements); y: f32 [tokens, m] with row stride
- * ldy.  accumulate=0 overwrites y, 1 adds to it.  k_splits=0 picks the K split
+ * ldy.  accumulate: 0 overwrites y, QIGEN_GEMV_ACCUMULATE adds to it, optionally
+ * or-ed with QIGEN_GEMV_X_READY (see above).  k_splits=0 picks the K split
  * automatically.  Deterministic: results do not depend on the launch shape
  * beyond (n, m, bits, group_size, tokens, k_splits).  Input sums are fused. */
 int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
@@ -121,6 +131,33 @@ int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, in
                   float* y, int64_t ldy, int accumulate, int k_splits, int prologue,
                   const float* prologue_w, float eps, void* workspace, int64_t workspace_bytes,
                   void* stream);
+
+/* ---- grouped GEMV: many independent GEMVs in one persistent launch ----------
+ * Replaces a sequence of independent qgemv(pm_i, x_i) calls of the reference
+ * runtime (e.g. its bench over a sweep of matrices,
+ * SPEC.md:418-426) by one schedule over all of them: one CTA per SM streams
+ * (GEMV, 128 columns, full K) work items back to back, so no per-GEMV launch
+ * latency or split-K reduction sits between them.  Each descriptor has the
+ * meaning of the qigen_gemv arguments (panel-layout weights, 1..2 activation
+ * rows).  Pointers are captured at create time; run() may be graph-captured.
+ * Results equal qigen_gemv's to f32 rounding (full-K reduction per column,
+ * deterministic). */
+typedef struct {
+  const uint32_t* qw;
+  const float* qsz;
+  int64_t n, m;
+  int bits;
+  int64_t group_size;
+  const void* x;
+  int x_dtype;
+  int64_t tokens, ldx;
+  float* y;
+  int64_t ldy;
+} qigen_gemv_desc;
+typedef struct qigen_gemv_group qigen_gemv_group;
+int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs, qigen_gemv_group** out);
+int qigen_gemv_group_run(const qigen_gemv_group* group, void* stream);
+int qigen_gemv_group_destroy(qigen_gemv_group* group);
 
 /* ---- decode-step glue (LLaMA driver) ----------------------------------------- */
 
@@ -149,13 +186,21 @@ int qigen_gemm_tc(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, in
  * %globaltimer stamps (entry, after the PDL wait, after the activation
  * prologue, after the main loop, exit, ...) to buf[(cta_y*grid_x + cta_x)*16 + i]. */
 int qigen_debug_trace(void* buf);
+/* Debugging aid: same points as qigen_debug_trace, SM clock64 values. */
+int qigen_debug_trace_clk(void* buf);
 /* Tuning aid: weight stages per warp issued before griddepcontrol.wait
  * (-1 = the whole first ring fill, the default). */
 int qigen_debug_prefetch(int stages_before_wait);
 /* Tuning aid: 1 = always digitise activations in the separate prep kernel. */
 int qigen_debug_force_prep(int on);
+/* Tuning aid: 1 = trigger the dependent launch (PDL) at GEMV kernel entry. */
+/* Tuning aid: L2 evict_first on weight copies, warps per CTA (8/16), ring KB per CTA, grid cap. */
+int qigen_debug_gemv_tuning(int policy, int wpc, int ring_kb, int max_ctas);
+int qigen_debug_early_trigger(int on);
 /* Tuning aid for the tensor-core path: 1 = skip A-tile stores, 2 = skip MMAs. */
 int qigen_debug_tc_mode(int mode);
+/* Tuning aid for the grouped GEMV: 1 = stream weights and activations only. */
+int qigen_debug_group_mode(int mode);
 
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
 

@@ -31,6 +31,13 @@ _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int
 
+class GemvDesc(ctypes.Structure):
+    """qigen_gemv_desc (include/qigen_b200.h)."""
+    _fields_ = [("qw", _P), ("qsz", _P), ("n", _I64), ("m", _I64), ("bits", _I32),
+                ("group_size", _I64), ("x", _P), ("x_dtype", _I32), ("tokens", _I64),
+                ("ldx", _I64), ("y", _P), ("ldy", _I64)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "qigen_version": (_I32, []),
@@ -51,15 +58,22 @@ SIGNATURES = {
     "qigen_gemv_workspace_size": (_I64, [_I64, _I64]),
     "qigen_gemv_ex": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64,
                              _I32, _I32, _I32, _P, ctypes.c_float, _P, _I64, _P]),
+    "qigen_gemv_group_create": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
+    "qigen_gemv_group_run": (_I32, [_P, _P]),
+    "qigen_gemv_group_destroy": (_I32, [_P]),
     "qigen_rope_kv": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "qigen_rmsnorm_f16": (_I32, [_P, _P, _I64, _I64, ctypes.c_float, _P, _P]),
     "qigen_gemm_tc_workspace_size": (_I64, [_I64, _I64]),
     "qigen_gemm_tc": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64, _I32,
                              _I32, _P, _I64, _P]),
     "qigen_debug_trace": (_I32, [_P]),
+    "qigen_debug_trace_clk": (_I32, [_P]),
     "qigen_debug_prefetch": (_I32, [_I32]),
     "qigen_debug_force_prep": (_I32, [_I32]),
+    "qigen_debug_early_trigger": (_I32, [_I32]),
+    "qigen_debug_gemv_tuning": (_I32, [_I32, _I32, _I32, _I32]),
     "qigen_debug_tc_mode": (_I32, [_I32]),
+    "qigen_debug_group_mode": (_I32, [_I32]),
     "qigen_weights_create": (_I32, [_P, _I32, _I64, _I64, _I32, _I64, _I64, _I64, _P, _I64,
                                     _P, _P, _P, ctypes.POINTER(_P)]),
     "qigen_weights_destroy": (_I32, [_P]),

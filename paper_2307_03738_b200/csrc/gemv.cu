@@ -34,6 +34,7 @@
 #include <utility>
 
 #include "common.cuh"
+#include "gemv_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -50,6 +51,7 @@ struct GemvArgs {
   int x_dtype;
   int x_vec;         // x rows 16-byte aligned -> vector loads
   int accumulate;
+  int x_ready;       // x is not written by the preceding kernel: read it before the PDL wait
   int max_steps;     // max K-steps (32 rows) of any chunk
   int D;             // ring stages per warp
   int pre;           // stages per warp issued before griddepcontrol.wait
@@ -60,6 +62,9 @@ struct GemvArgs {
   unsigned char* ws;          // caller workspace for `dig` (may be null)
   size_t ws_bytes;
   unsigned long long* trace;  // optional per-CTA timestamps (qigen_debug_trace)
+  unsigned long long* trace_clk;  // optional per-CTA SM clocks at the same points
+  int early;                  // trigger dependents at kernel entry
+  int policy;                 // 1: weight bulk copies carry an L2 evict_first hint
 };
 
 __device__ __forceinline__ void trace_point(const GemvArgs& a, int i) {
@@ -67,122 +72,10 @@ __device__ __forceinline__ void trace_point(const GemvArgs& a, int i) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + i] = t;
+    if (a.trace_clk) a.trace_clk[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + i] = clock64();
   }
 }
 
-// ---- PTX helpers -------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_addr(bar);
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
-// Cluster address of the same shared-memory offset in CTA `rank`.
-__device__ __forceinline__ uint32_t mapa(const void* p, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
-  return r;
-}
-// 4-byte store into another CTA's shared memory, completing tx on its mbarrier.
-__device__ __forceinline__ void st_async(uint32_t addr, float v, uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
-                   addr),
-               "r"(__float_as_uint(v)), "r"(bar)
-               : "memory");
-}
-
-__device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint2 b) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
-}
-
-// Fragment registers of local step sl (0..7) from the lane's superstep words.
-// Codes stay in place (one AND each); every accumulator row then carries a
-// power-of-two scale: RowScale<BITS>::hi for rows gq+8 (rows gq: 1), and for
-// 2-bit odd steps a further x16 on both rows (kept in the odd accumulator set).
-template <int BITS>
-__device__ __forceinline__ void extract(const uint4 (&w)[BITS], int sl, uint32_t (&a)[4]);
-
-template <>
-__device__ __forceinline__ void extract<4>(const uint4 (&w)[4], int sl, uint32_t (&a)[4]) {
-  const uint4 u = w[sl >> 1];
-  const uint32_t A = (sl & 1) ? u.z : u.x, B = (sl & 1) ? u.w : u.y;
-  a[0] = A & 0x0F0F0F0Fu;  // rows gq,   k 4t..      x1
-  a[1] = A & 0xF0F0F0F0u;  // rows gq+8, k 4t..      x16
-  a[2] = B & 0x0F0F0F0Fu;  // rows gq,   k 16+4t..   x1
-  a[3] = B & 0xF0F0F0F0u;  // rows gq+8, k 16+4t..   x16
-}
-
-template <>
-__device__ __forceinline__ void extract<2>(const uint4 (&w)[2], int sl, uint32_t (&a)[4]) {
-  const uint4 u = w[sl >> 2];
-  const int q = sl & 2;  // word pair of this step pair
-  const uint32_t X = q == 0 ? u.x : u.z, Y = q == 0 ? u.y : u.w;
-  const uint32_t m0 = (sl & 1) ? 0x30303030u : 0x03030303u;  // x1  (odd: x16)
-  const uint32_t m1 = (sl & 1) ? 0xC0C0C0C0u : 0x0C0C0C0Cu;  // x4  (odd: x64)
-  a[0] = X & m0;
-  a[1] = X & m1;
-  a[2] = Y & m0;
-  a[3] = Y & m1;
-}
-
-__device__ __forceinline__ uint32_t word_of(const uint4 (&w)[3], int q) {
-  const uint4 u = w[q >> 2];
-  const int c = q & 3;
-  return c == 0 ? u.x : c == 1 ? u.y : c == 2 ? u.z : u.w;
-}
-
-template <>
-__device__ __forceinline__ void extract<3>(const uint4 (&w)[3], int sl, uint32_t (&a)[4]) {
-  const int pi = sl >> 1;
-  const uint32_t A = word_of(w, 3 * pi), B = word_of(w, 3 * pi + 1), C = word_of(w, 3 * pi + 2);
-  if ((sl & 1) == 0) {
-    a[0] = A & 0x07070707u;  // x1
-    a[1] = A & 0x38383838u;  // x8
-    a[2] = B & 0x07070707u;
-    a[3] = B & 0x38383838u;
-  } else {
-    a[0] = C & 0x07070707u;
-    a[1] = C & 0x38383838u;
-    a[2] = ((A >> 6) & 0x03030303u) | ((C >> 4) & 0x04040404u);  // x1
-    a[3] = ((B >> 3) & 0x18181818u) | ((C >> 2) & 0x20202020u);  // x8
-  }
-}
-
-template <int BITS>
-struct RowScale {  // scale of the rows gq+8 accumulators relative to rows gq
-  static constexpr float inv_hi = BITS == 4 ? 1.f / 16.f : BITS == 3 ? 1.f / 8.f : 1.f / 4.f;
-};
-
-__device__ __forceinline__ int sbyte(int v) { return (int)(int8_t)(v & 0xFF); }
 
 // Four consecutive raw activations (row element offset `base`, `k` = column) as
 // f32, zero beyond n.
@@ -233,64 +126,6 @@ __device__ __forceinline__ void load_x4(const GemvArgs& a, int tk, int64_t k, fl
   }
 }
 
-// ---- activation digitisation (shared by the fused prologue and the prep kernel)
-// An "item" is 4 consecutive rows of one token.  IPU consecutive lanes hold one
-// exponent unit (U = min(g, 128) rows); they agree on E (max |x| < 2^E) with one
-// REDUX, split m = rint(x 2^(30-E)) into balanced signed bytes, and reduce the
-// exact unit sum of m.  Returns the four digit words (d0..d3 of the 4 rows).
-struct Digits {
-  uint32_t dw[4];
-  float xsum;   // sum of m over the unit (valid in every lane of the unit)
-  float scale;  // 2^(E-30)
-};
-
-template <int IPU>
-__device__ __forceinline__ Digits digitize(const float (&v)[4], uint32_t umask) {
-  Digits d;
-  const float m4 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
-  const uint32_t umx = __reduce_max_sync(umask, __float_as_uint(m4));
-  // max < 2^e; e from the biased exponent (denormal max: 2^-126 still bounds it)
-  const int e = umx ? (int)((umx >> 23) & 0xFF) - 126 : 0;
-  const int k = 30 - e, k1 = k >> 1, k2 = k - k1;  // 2^k may leave the f32 range
-  const float f1 = __int_as_float((127 + k1) << 23), f2 = __int_as_float((127 + k2) << 23);
-  int mv[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) mv[i] = __float2int_rn(__fmul_rn(__fmul_rn(v[i], f1), f2));
-  // balanced base-256 digits: with t = m + 0x808080, digit j < 3 is byte j of t
-  // minus 128 (i.e. byte ^ 0x80 as s8) and the top digit is t >> 24 (|.| <= 64)
-  uint32_t tt[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) tt[i] = (uint32_t)(mv[i] + 0x808080);
-  const uint32_t lo01 = __byte_perm(tt[0], tt[1], 0x5140), lo23 = __byte_perm(tt[2], tt[3], 0x5140);
-  const uint32_t hi01 = __byte_perm(tt[0], tt[1], 0x7362), hi23 = __byte_perm(tt[2], tt[3], 0x7362);
-  d.dw[3] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // byte 0 of each
-  d.dw[2] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // byte 1
-  d.dw[1] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // byte 2
-  d.dw[0] = __byte_perm(hi01, hi23, 0x7632);                // byte 3 = t >> 24
-  // exact unit sum of m, split 16/16 so each half fits an int32 REDUX
-  int slo = 0, shi = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    slo += mv[i] & 0xFFFF;
-    shi += mv[i] >> 16;
-  }
-  slo = __reduce_add_sync(umask, slo);
-  shi = __reduce_add_sync(umask, shi);
-  d.xsum = fmaf((float)shi, 65536.f, (float)slo);
-  d.scale = umx ? __int_as_float((127 + e - 30) << 23) : 0.f;  // e - 30 >= -156: see below
-  if (umx && e - 30 < -126) d.scale = scalbnf(1.f, e - 30);
-  return d;
-}
-
-// Digit store: B-fragment words of (step st, token tk) at [st][TP][j][t] x (b0, b1).
-__device__ __forceinline__ void store_digits(uint32_t* base, int st, int tk, int TP, int sub,
-                                             const Digits& d) {
-  uint32_t* dst = base + ((st * TP + tk) * 16 + (sub & 3)) * 2 + (sub >> 2);
-  dst[0] = d.dw[0];
-  dst[8] = d.dw[1];
-  dst[16] = d.dw[2];
-  dst[24] = d.dw[3];
-}
 
 // 1/rms over the full rows of tokens [t0, t0 + ntok) (RMSNorm prologue),
 // block-wide; inv[tk - t0].
@@ -379,7 +214,7 @@ struct SmemLayout {
 // fixed-point exponent (found with one REDUX, no CTA barrier), and the integer
 // accumulators are folded into f32 once per unit.
 template <int BITS, int NB, int WPC, int GPS>
-__global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int T = WPC * 32;
   constexpr int TP = 2 * NB;                // tokens in the fragment layout (padded)
@@ -405,14 +240,22 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
 
   const char* wsrc = (const char*)(a.qw + ((int64_t)(active ? p : 0) * a.KS) * BITS * 32);
   const char* zsrc = (const char*)(a.qsz + (int64_t)(active ? p : 0) * a.Gp * 16);
+  uint64_t pol = 0;
+  if (a.policy) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   auto issue = [&](int s) {  // lane 0: superstep s of the chunk into slot s % D
     const int slot = s % D;
     unsigned char* dst = ring + slot * L.stage;
     mbar_expect_tx(&bars[slot], (uint32_t)L.stage);
-    bulk_g2s(dst, wsrc + (int64_t)(ks0 + s) * BITS * 512, BITS * 512, &bars[slot]);
-    if (SZB) bulk_g2s(dst + BITS * 512, zsrc + (int64_t)(ks0 + s) * SZB, SZB, &bars[slot]);
+    if (a.policy) {
+      bulk_g2s_hint(dst, wsrc + (int64_t)(ks0 + s) * BITS * 512, BITS * 512, &bars[slot], pol);
+      if (SZB) bulk_g2s_hint(dst + BITS * 512, zsrc + (int64_t)(ks0 + s) * SZB, SZB, &bars[slot], pol);
+    } else {
+      bulk_g2s(dst, wsrc + (int64_t)(ks0 + s) * BITS * 512, BITS * 512, &bars[slot]);
+      if (SZB) bulk_g2s(dst + BITS * 512, zsrc + (int64_t)(ks0 + s) * SZB, SZB, &bars[slot]);
+    }
   };
   trace_point(a, 0);
+  if (a.early) asm volatile("griddepcontrol.launch_dependents;");
 
   // ---- 1. ring setup + weight prefetch (independent of the previous kernel) --
   const int n_first = active ? min(D, nks) : 0;
@@ -454,7 +297,10 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   __syncthreads();
 
   // ---- 2. PDL: everything below may read what the previous kernel wrote -----
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // (with x_ready the inputs are known not to come from the preceding kernel:
+  // only the y write below waits, so this GEMV overlaps its predecessor fully)
+  const bool early_x = a.x_ready && !a.dig;
+  if (!early_x) asm volatile("griddepcontrol.wait;" ::: "memory");
   trace_point(a, 1);
 
   // ---- 3. activation digits for this chunk into shared memory ----------------
@@ -495,6 +341,7 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
           for (int s = n_pre; s < n_first; ++s) issue(s);
       }
       const Digits d = digitize<IPU>(v, umask);
+      if (it0 == 0) trace_point(a, 11);
       if (live) {
         store_digits(bw, st, tk, TP, sub, d);
         if ((it % IPU) == 0) xs[((it % (nsteps * 8)) / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
@@ -512,7 +359,7 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
     trace_point(a, 10);
     __syncthreads();
   }
-  asm volatile("griddepcontrol.launch_dependents;");
+  if (!a.early) asm volatile("griddepcontrol.launch_dependents;");
   trace_point(a, 2);
 
   // ---- 4. main loop ------------------------------------------------------------
@@ -628,6 +475,7 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
   trace_point(a, 6);
   const int64_t col0 = (int64_t)blockIdx.x * WPC * 16;
   if (rank == 0 && S > 1) mbar_wait(rbar, 0);
+  if (early_x && rank == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before y
   trace_point(a, 7);
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
@@ -658,9 +506,15 @@ __global__ void __launch_bounds__(WPC * 32, 512 / (WPC * 32)) gemv_kernel(const 
 
 // ---------------------------------------------------------------------------
 unsigned long long* g_trace = nullptr;  // shared with gemm_tc.cu
+static unsigned long long* g_trace_clk = nullptr;
 constexpr int kMaxSplits = 16;  // cluster size along K (non-portable above 8)
 static int g_pre = -1;  // stages issued before the PDL wait (-1: all of the first fill)
 static int g_force_prep = 0;  // tuning: always digitise activations in act_prep_kernel
+static int g_early = 0;       // tuning: trigger the dependent launch at kernel entry
+static int g_policy = 0;      // tuning: L2 evict_first hint on weight copies
+static int g_wpc = 8;         // tuning: warps per CTA for <= 4 tokens (8 or 16)
+static int g_ring_kb = 0;     // tuning: ring bytes per CTA (KB; 0 = 10 KB per warp)
+static int g_max_ctas = 0;    // tuning: cap on the grid (0 = rule below)
 
 static int sm_count() {
   static int cached = 0;
@@ -714,7 +568,8 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     const int max_ks = (a.KS + S - 1) / S;
     a.max_steps = max_ks * 8;
     SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, TP, a.M, WPC, S);
-    const int budget = std::min(WPC * 10 * 1024, 224 * 1024 - L0.total - WPC * 16);
+    const int budget = std::min(g_ring_kb ? g_ring_kb * 1024 : WPC * 10 * 1024,
+                                224 * 1024 - L0.total - WPC * 16);
     a.D = std::max(2, std::min(max_ks, budget / (WPC * stage)));
     return SmemLayout(BITS, GPS * 128, a.D, a.max_steps, TP, a.M, WPC, S);
   };
@@ -758,6 +613,12 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
         S = c;
       }
     }
+  }
+  if (req_S <= 0 && g_max_ctas > 0) {
+    // tuning: the largest split whose grid stays within the cap
+    S = 1;
+    for (int c = 2; c <= std::min(kMaxSplits, a.KS); ++c)
+      if (cols * c <= g_max_ctas && (a.KS + c - 1) / c >= 2) S = c;
   }
   QIGEN_CHECK_ARG(S >= 1 && S <= a.KS && S <= kMaxSplits, QIGEN_ERR_ARG, "k_splits %d out of range", S);
   // many tokens x long chunks: split K further until the fragments fit in smem
@@ -829,8 +690,12 @@ static int launch_nb(GemvArgs& a, int S, cudaStream_t stream) {
   const int nb = (a.M + 1) / 2;
   if (nb <= 1) return launch_gps<BITS, 1, WPC>(a, S, stream);
   if (nb <= 2) return launch_gps<BITS, 2, WPC>(a, S, stream);
-  if (nb <= 4) return launch_gps<BITS, 4, WPC>(a, S, stream);
-  return launch_gps<BITS, 8, WPC>(a, S, stream);
+  if constexpr (WPC > 8) {
+    return QIGEN_ERR_ARG;
+  } else {
+    if (nb <= 4) return launch_gps<BITS, 4, WPC>(a, S, stream);
+    return launch_gps<BITS, 8, WPC>(a, S, stream);
+  }
 }
 
 }  // namespace qigen
@@ -844,6 +709,24 @@ extern "C" int qigen_debug_trace(void* buf) {
 
 extern "C" int qigen_debug_prefetch(int stages_before_wait) {
   g_pre = stages_before_wait;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_trace_clk(void* buf) {
+  g_trace_clk = (unsigned long long*)buf;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_early_trigger(int on) {
+  g_early = on;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_gemv_tuning(int policy, int wpc, int ring_kb, int max_ctas) {
+  g_policy = policy;
+  g_wpc = wpc;
+  g_ring_kb = ring_kb;
+  g_max_ctas = max_ctas;
   return QIGEN_OK;
 }
 
@@ -902,11 +785,16 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   a.ws_bytes = workspace ? (size_t)workspace_bytes : 0;
   a.xw = prologue_w;
   a.eps = eps;
-  a.accumulate = accumulate;
+  a.accumulate = accumulate & QIGEN_GEMV_ACCUMULATE;
+  a.x_ready = (accumulate & QIGEN_GEMV_X_READY) ? 1 : 0;
   a.trace = g_trace;
+  a.trace_clk = g_trace_clk;
+  a.early = g_early || a.x_ready;  // independent x: overlap the predecessor fully
+  a.policy = g_policy;
   const int S = k_splits;  // 0: chosen per launch shape in launch_cfg
   cudaStream_t s = (cudaStream_t)stream;
-#define QIGEN_LAUNCH(B) return launch_nb<B, 8>(a, S, s)
+#define QIGEN_LAUNCH(B) \
+  return (g_wpc == 16 && tokens <= 4) ? launch_nb<B, 16>(a, S, s) : launch_nb<B, 8>(a, S, s)
   switch (bits) {
     case 2: QIGEN_LAUNCH(2);
     case 3: QIGEN_LAUNCH(3);

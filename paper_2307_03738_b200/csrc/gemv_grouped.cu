@@ -1,0 +1,498 @@
+// Grouped batch-1 GEMV: many INDEPENDENT quantized GEMVs (mixed bits / group
+// sizes / shapes) in one persistent launch.
+//
+// Same arithmetic as the split-K GEMV (gemv.cu; the reference factorisation
+// kernelgen.py:227-240 with exact IMMA partials), different schedule.  A chain
+// of single GEMVs pays, per launch, the programmatic-launch release, the
+// activation prologue and the split-K reduction on the critical path (DESIGN.md
+// §4).  When the GEMVs are independent (the reference runtime's per-matrix
+// qgemv calls of a sweep; the BASELINE configs[1] workload) a
+// persistent schedule hides all of it:
+//   * one CTA per SM, 16 consumer warps + 1 producer warp;
+//   * a work item is one GEMV x 16 panels (256 output columns) x the FULL K
+//     range, so every output column is reduced by exactly one warp in a fixed
+//     order: deterministic, no split-K, no atomics, no cross-CTA traffic;
+//   * items are assigned to CTAs on the host by longest-processing-time-first
+//     greedy on their byte counts (a static, reproducible balance);
+//   * each consumer warp streams its panel of every item of its CTA through its
+//     own ring of TMA bulk-copy stages, issuing ahead ACROSS item boundaries, so
+//     the weight stream never drains between GEMVs;
+//   * the activations of all GEMVs are digitised once by group_prep_kernel into
+//     per-superstep records (digits + unit sums/exponents) which the producer
+//     warp streams through a CTA-shared ring, behind the PDL wait on the prep
+//     kernel (the weight prefetch is issued before it).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <queue>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "gemv_common.cuh"
+
+namespace qigen {
+
+constexpr int kGWarps = 16;            // consumer warps per CTA (panels per item)
+constexpr int kGTP = 2;                // tokens in the fragment layout (M <= 2)
+constexpr int kRecDig = 8 * kGTP * 128;  // digit bytes per superstep record
+constexpr int kRecBytes = kRecDig + 8 * kGTP * 8;  // + (xsum, 2^(E-30)) per unit
+constexpr int kGSlot = 4 * 512 + 8 * 128;  // largest weight stage (4-bit, g = 32)
+constexpr int kGDepth = 4;                 // weight stages per consumer warp
+constexpr int kGRecDepth = 8;              // activation records in the CTA ring
+
+struct GDesc {
+  const uint4* qw;
+  const float2* qsz;
+  const void* x;
+  float* y;
+  int64_t ldx, ldy, n, m;
+  int KS, P, Gp, g, bits, gps, M, x_dtype;
+  int64_t rec0;  // index of this GEMV's first superstep record in the workspace
+};
+struct GItem {
+  int d, p0;
+};
+struct GPlan {
+  const GDesc* desc;
+  const GItem* items;
+  const int* cta_start;  // [grid + 1]
+  unsigned char* rec;    // activation records
+  int count;
+  int mode;              // tuning: 1 = stream only (no compute)
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Four consecutive activations of token tk (zero beyond n / for padding tokens).
+__device__ __forceinline__ void gload4(const GDesc& d, int tk, int64_t k, float (&v)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float f = 0.f;
+    if (tk < d.M && k + i < d.n) {
+      const int64_t o = tk * d.ldx + k + i;
+      if (d.x_dtype == QIGEN_F32) f = __ldg((const float*)d.x + o);
+      else if (d.x_dtype == QIGEN_F16) f = __half2float(((const __half*)d.x)[o]);
+      else f = __bfloat162float(((const __nv_bfloat16*)d.x)[o]);
+    }
+    v[i] = f;
+  }
+}
+
+template <int IPU>
+__device__ __forceinline__ void group_prep_item(const GPlan& pl, const GDesc& d, int it) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
+  const bool live = it < d.KS * 64;
+  const int st = it >> 3, sub = it & 7;
+  const int sup = st >> 3, sl = st & 7;
+  unsigned char* rec = pl.rec + (size_t)(d.rec0 + (live ? sup : 0)) * kRecBytes;
+#pragma unroll
+  for (int tk = 0; tk < kGTP; ++tk) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (live) gload4(d, tk, (int64_t)32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v);
+    const Digits dg = digitize<IPU>(v, umask);
+    if (live) {
+      store_digits((uint32_t*)rec, sl, tk, kGTP, sub, dg);
+      if ((it % IPU) == 0) {
+        const int uj = (it % 64) / IPU;
+        ((float2*)(rec + kRecDig))[uj * kGTP + tk] =
+            tk < d.M ? make_float2(dg.xsum, dg.scale) : make_float2(0.f, 0.f);
+      }
+    }
+  }
+}
+
+// Activation records of every GEMV of the group; grid (ceil(max KS*64/256), count).
+__global__ void __launch_bounds__(256) group_prep_kernel(const GPlan pl) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const GDesc& d = pl.desc[blockIdx.y];
+  if ((int)blockIdx.x * 256 >= d.KS * 64) return;
+  const int it = blockIdx.x * 256 + threadIdx.x;
+  const int U = d.g == 32 ? 32 : d.g == 64 ? 64 : 128;  // exponent unit (rows)
+  if (U == 32) group_prep_item<8>(pl, d, it);
+  else if (U == 64) group_prep_item<16>(pl, d, it);
+  else group_prep_item<32>(pl, d, it);
+}
+
+// IMMA with a zero accumulator input (first step of a chain in a unit).
+__device__ __forceinline__ void imma0(int (&c)[4], const uint32_t (&a)[4], uint2 b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};"
+      : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y), "r"(0));
+}
+
+// Accumulate one 256-row superstep of one panel: 8 IMMA steps + unit flushes.
+// w: the lane's weight words; szs: (s, z) of the groups of this superstep;
+// rec: the activation record of this superstep.
+template <int BITS, int GPS>
+__device__ __forceinline__ void group_superstep(const uint4 (&w)[BITS], const float2* szs,
+                                                const unsigned char* rec, float (&yv)[2]) {
+  constexpr int UPS = GPS > 2 ? GPS : 2;
+  constexpr int SPU = 8 / UPS;
+  const int lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
+  const uint2* bs = (const uint2*)rec + (gq >> 2) * 16 + (gq & 3) * 4 + t;
+  const float2* xs = (const float2*)(rec + kRecDig);
+  const float w_lo = (t & 1) ? 1.f : 65536.f;
+  const float w_hi = w_lo * RowScale<BITS>::inv_hi;
+  const bool xon = (t & 1) == 0;
+  int acc[2][4];
+#pragma unroll
+  for (int sl = 0; sl < 8; ++sl) {
+    uint32_t af[4];
+    extract<BITS>(w, sl, af);
+    // a chain starts from zero at its first step in the unit (no reset moves)
+    if (sl % SPU < 2) imma0(acc[sl & 1], af, bs[sl * kGTP * 16]);
+    else imma(acc[sl & 1], af, bs[sl * kGTP * 16]);
+    if ((sl + 1) % SPU == 0) {
+      const int uj = (sl + 1) / SPU - 1;
+      const int gi = GPS >= UPS ? uj : 0;
+      const float2 sz0 = szs[gi * 16 + gq], sz1 = szs[gi * 16 + gq + 8];
+      const float2 xv = xs[uj * kGTP + (t >> 1)];
+      const float X = xon ? xv.x : 0.f, sc = xv.y;
+      constexpr int sh = BITS == 2 ? 4 : 0;  // 2-bit odd steps carry an extra x16
+      int c0, c1, c2, c3;
+      if (SPU == 1) {  // one step per unit: only its chain holds data
+        const int k = sl & 1, shk = k ? sh : 0;
+        c0 = acc[k][0] >> shk; c1 = acc[k][1] >> shk; c2 = acc[k][2] >> shk; c3 = acc[k][3] >> shk;
+      } else {
+        c0 = acc[0][0] + (acc[1][0] >> sh); c1 = acc[0][1] + (acc[1][1] >> sh);
+        c2 = acc[0][2] + (acc[1][2] >> sh); c3 = acc[0][3] + (acc[1][3] >> sh);
+      }
+      const float q0 = (float)(c0 * 256 + c1), q1 = (float)(c2 * 256 + c3);
+      yv[0] = fmaf(sz0.x * sc, fmaf(-sz0.y, X, q0 * w_lo), yv[0]);
+      yv[1] = fmaf(sz1.x * sc, fmaf(-sz1.y, X, q1 * w_hi), yv[1]);
+    }
+  }
+}
+
+__device__ __forceinline__ int gcombo(const GDesc& d) { return (d.bits - 2) * 5 + d.gps; }
+
+__global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const GPlan pl) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* rring = smem + kGWarps * kGDepth * kGSlot;           // [DD][record]
+  uint64_t* wfull = (uint64_t*)(rring + kGRecDepth * kRecBytes);      // [warp][D]
+  uint64_t* rfull = wfull + kGWarps * kGDepth;                        // [DD]
+  uint64_t* rempty = rfull + kGRecDepth;
+  const int i0 = pl.cta_start[blockIdx.x], i1 = pl.cta_start[blockIdx.x + 1];
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGWarps * kGDepth; ++i) mbar_init(&wfull[i], 1);
+    for (int i = 0; i < kGRecDepth; ++i) {
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], kGWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kGWarps) {
+    // ---- activation-record producer (after the PDL wait on the prep kernel)
+    if (lane == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int it = i0; it < i1; ++it) {
+        const GDesc& d = pl.desc[pl.items[it].d];
+        // fields in registers: the asm memory clobbers below would otherwise
+        // force a global reload per record
+        const int KS = d.KS;
+        const unsigned char* src = pl.rec + (size_t)d.rec0 * kRecBytes;
+        for (int s = 0; s < KS; ++s) {
+          mbar_wait(&rempty[slot], ph ^ 1u);
+          mbar_expect_tx(&rfull[slot], kRecBytes);
+          bulk_g2s(rring + slot * kRecBytes, src + (size_t)s * kRecBytes, kRecBytes, &rfull[slot]);
+          if (++slot == kGRecDepth) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warp: panel p0 + warp of every item of this CTA ---------------
+  unsigned char* ring = smem + warp * kGDepth * kGSlot;
+  uint64_t* full = wfull + warp * kGDepth;
+  // Issue cursor (lane 0) over this warp's (item, superstep) stream, skipping
+  // items in which the warp has no panel (ragged last item of a GEMV); the
+  // current item's stream geometry is cached in registers.
+  int ci = i0, cs = 0, issued = 0;
+  int c_ks = 0, c_gps = 0, c_g = 0;
+  uint32_t c_wb = 0, c_zb = 0;
+  const char *c_w = nullptr, *c_z = nullptr;
+  auto load_item = [&]() {
+    while (ci < i1) {
+      const GItem itm = pl.items[ci];
+      const GDesc& d = pl.desc[itm.d];
+      const int p = itm.p0 + warp;
+      if (p < d.P) {
+        c_ks = d.KS;
+        c_gps = d.gps;
+        c_g = d.g;
+        c_wb = d.bits * 512;
+        c_zb = (d.gps > 0 ? d.gps : 1) * 128;
+        c_w = (const char*)d.qw + (int64_t)p * d.KS * c_wb;
+        c_z = (const char*)(d.qsz + (int64_t)p * d.Gp * 16);
+        return;
+      }
+      ++ci;
+    }
+  };
+  auto issue_one = [&]() {  // next stage of the stream into slot issued % D
+    const int slot = issued % kGDepth;
+    const int64_t gfirst = c_gps > 0 ? (int64_t)cs * c_gps : (c_g ? (int64_t)cs * kSuper / c_g : 0);
+    mbar_expect_tx(&full[slot], c_wb + c_zb);
+    bulk_g2s(ring + slot * kGSlot, c_w + (int64_t)cs * c_wb, c_wb, &full[slot]);
+    bulk_g2s(ring + slot * kGSlot + c_wb, c_z + gfirst * 128, c_zb, &full[slot]);
+    ++issued;
+    if (++cs == c_ks) {
+      ++ci;
+      cs = 0;
+      load_item();
+    }
+  };
+  if (lane == 0) {
+    load_item();
+    while (ci < i1 && issued < kGDepth) issue_one();
+  }
+  __syncwarp();
+
+  int consumed = 0, rn = 0;
+  bool waited = false;
+  for (int it = i0; it < i1; ++it) {
+    const GItem itm = pl.items[it];
+    const GDesc& d = pl.desc[itm.d];
+    const int p = itm.p0 + warp;
+    const bool active = p < d.P;
+    const int combo = gcombo(d);
+    const int KS = d.KS;  // registers (see the producer)
+    float yv[2] = {0.f, 0.f};
+    for (int s = 0; s < KS; ++s) {
+      const int rs = rn % kGRecDepth;
+      mbar_wait(&rfull[rs], (uint32_t)(rn / kGRecDepth) & 1u);
+      if (active) {
+        const int slot = consumed % kGDepth;
+        mbar_wait(&full[slot], (uint32_t)(consumed / kGDepth) & 1u);
+        const unsigned char* stg = ring + slot * kGSlot;
+        const unsigned char* rec = rring + rs * kRecBytes;
+        if (pl.mode != 1) {
+          switch (combo) {
+#define QG_CASE(B, G)                                                               \
+  case (B - 2) * 5 + G: {                                                           \
+    uint4 w[B];                                                                     \
+    _Pragma("unroll") for (int v = 0; v < B; ++v) w[v] = ((const uint4*)stg)[v * 32 + lane]; \
+    group_superstep<B, G>(w, (const float2*)(stg + B * 512), rec, yv);              \
+  } break;
+            QG_CASE(2, 0) QG_CASE(2, 1) QG_CASE(2, 2) QG_CASE(2, 4) QG_CASE(2, 8)
+            QG_CASE(3, 0) QG_CASE(3, 1) QG_CASE(3, 2) QG_CASE(3, 4) QG_CASE(3, 8)
+            QG_CASE(4, 0) QG_CASE(4, 1) QG_CASE(4, 2) QG_CASE(4, 4) QG_CASE(4, 8)
+#undef QG_CASE
+            default: break;
+          }
+        }
+        ++consumed;
+        __syncwarp();
+        if (lane == 0 && ci < i1) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue_one();
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rempty[rs]);
+      ++rn;
+    }
+    if (active) {
+      const int gq = lane >> 2, t = lane & 3;
+      const float v0 = yv[0] + __shfl_xor_sync(0xffffffffu, yv[0], 1);
+      const float v1 = yv[1] + __shfl_xor_sync(0xffffffffu, yv[1], 1);
+      const int tk = t >> 1;
+      if (!waited) {  // y may be read or written by the preceding kernel
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+      }
+      if ((t & 1) == 0 && tk < d.M) {
+        const int64_t c0 = (int64_t)p * 16 + gq;
+        if (c0 < d.m) d.y[tk * d.ldy + c0] = v0;
+        if (c0 + 8 < d.m) d.y[tk * d.ldy + c0 + 8] = v1;
+      }
+    }
+  }
+}
+
+constexpr int kGSmem = kGWarps * kGDepth * kGSlot + kGRecDepth * kRecBytes +
+                       (kGWarps * kGDepth + 2 * kGRecDepth) * 8;
+
+}  // namespace qigen
+
+using namespace qigen;
+
+struct qigen_gemv_group {
+  void* blob = nullptr;  // device: descs | items | cta_start
+  unsigned char* rec = nullptr;
+  GPlan plan{};
+  int grid = 0, max_ks = 0;
+};
+
+extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
+                                       qigen_gemv_group** out) {
+  QIGEN_CHECK_ARG(out && descs && count > 0, QIGEN_ERR_ARG, "bad group arguments");
+  std::vector<GDesc> ds(count);
+  int64_t recs = 0;
+  int max_ks = 0;
+  for (int i = 0; i < count; ++i) {
+    const qigen_gemv_desc& e = descs[i];
+    QIGEN_CHECK_ARG(e.bits == 2 || e.bits == 3 || e.bits == 4, QIGEN_ERR_CONFIG,
+                    "gemv %d: bits must be one of (2, 3, 4), got %d", i, e.bits);
+    QIGEN_CHECK_ARG(e.qw && e.qsz && e.x && e.y && e.n > 0 && e.m > 0, QIGEN_ERR_ARG,
+                    "gemv %d: null pointer or empty matrix", i);
+    QIGEN_CHECK_ARG(e.group_size == 0 || e.n % e.group_size == 0, QIGEN_ERR_CONFIG,
+                    "gemv %d: group size %lld does not divide row count %lld", i,
+                    (long long)e.group_size, (long long)e.n);
+    QIGEN_CHECK_ARG(e.group_size == 0 || e.group_size == 32 || e.group_size == 64 ||
+                        e.group_size == 128 || e.group_size % kSuper == 0,
+                    QIGEN_ERR_UNSUPPORTED, "gemv %d: unsupported group size %lld", i,
+                    (long long)e.group_size);
+    QIGEN_CHECK_ARG(e.tokens >= 1 && e.tokens <= kGTP, QIGEN_ERR_UNSUPPORTED,
+                    "gemv %d: the grouped GEMV takes 1 or 2 activation rows", i);
+    QIGEN_CHECK_ARG(e.x_dtype >= 0 && e.x_dtype <= 2, QIGEN_ERR_ARG, "gemv %d: bad x dtype", i);
+    QIGEN_CHECK_ARG(e.ldx >= e.n && e.ldy >= e.m, QIGEN_ERR_ARG, "gemv %d: leading dimensions", i);
+    GDesc& d = ds[i];
+    d.qw = (const uint4*)e.qw;
+    d.qsz = (const float2*)e.qsz;
+    d.x = e.x;
+    d.y = e.y;
+    d.ldx = e.ldx;
+    d.ldy = e.ldy;
+    d.n = e.n;
+    d.m = e.m;
+    d.KS = (int)supersteps(e.n);
+    d.P = (int)panels(e.m);
+    d.Gp = (int)groups_padded(e.n, e.group_size);
+    d.g = (int)e.group_size;
+    d.bits = e.bits;
+    d.gps = e.group_size == 32 ? 8 : e.group_size == 64 ? 4 : e.group_size == 128 ? 2
+            : e.group_size == 256 ? 1 : 0;
+    d.M = (int)e.tokens;
+    d.x_dtype = e.x_dtype;
+    d.rec0 = recs;
+    recs += d.KS;
+    max_ks = std::max(max_ks, d.KS);
+  }
+  // items (GEMV x 16 panels x full K) and their stream bytes
+  std::vector<GItem> items;
+  std::vector<double> cost;
+  for (int i = 0; i < count; ++i) {
+    const GDesc& d = ds[i];
+    for (int p0 = 0; p0 < d.P; p0 += kGWarps) {
+      const int act = std::min(kGWarps, d.P - p0);
+      items.push_back({i, p0});
+      const int zb = (d.gps > 0 ? d.gps : 1) * 128;
+      cost.push_back((double)d.KS * (act * (d.bits * 512 + zb) + kRecBytes));
+    }
+  }
+  int dev = 0, sms = 148;
+  QIGEN_CUDA_RET(cudaGetDevice(&dev));
+  QIGEN_CUDA_RET(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::max(1, std::min<int>(sms, (int)items.size()));
+  // longest-processing-time-first greedy: biggest item to the least-loaded CTA
+  std::vector<int> order(items.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  using Load = std::pair<double, int>;
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (int c = 0; c < grid; ++c) heap.push({0.0, c});
+  std::vector<std::vector<int>> per(grid);
+  for (int i : order) {
+    Load l = heap.top();
+    heap.pop();
+    per[l.second].push_back(i);
+    heap.push({l.first + cost[i], l.second});
+  }
+  std::vector<GItem> flat;
+  std::vector<int> start(grid + 1, 0);
+  for (int c = 0; c < grid; ++c) {
+    start[c] = (int)flat.size();
+    for (int i : per[c]) flat.push_back(items[i]);
+  }
+  start[grid] = (int)flat.size();
+
+  auto* g = new qigen_gemv_group();
+  const size_t db = ds.size() * sizeof(GDesc), ib = flat.size() * sizeof(GItem),
+               sb = start.size() * sizeof(int);
+  const size_t ib_off = (db + 255) / 256 * 256, sb_off = ib_off + (ib + 255) / 256 * 256;
+  cudaError_t e1 = cudaMalloc(&g->blob, sb_off + sb);
+  cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc((void**)&g->rec, (size_t)recs * kRecBytes) : e1;
+  if (e2 != cudaSuccess) {
+    if (g->blob) cudaFree(g->blob);
+    delete g;
+    QIGEN_CUDA_RET(e2);
+  }
+  char* b = (char*)g->blob;
+  QIGEN_CUDA_RET(cudaMemcpy(b, ds.data(), db, cudaMemcpyHostToDevice));
+  QIGEN_CUDA_RET(cudaMemcpy(b + ib_off, flat.data(), ib, cudaMemcpyHostToDevice));
+  QIGEN_CUDA_RET(cudaMemcpy(b + sb_off, start.data(), sb, cudaMemcpyHostToDevice));
+  g->plan.desc = (const GDesc*)b;
+  g->plan.items = (const GItem*)(b + ib_off);
+  g->plan.cta_start = (const int*)(b + sb_off);
+  g->plan.rec = g->rec;
+  g->plan.count = count;
+  g->plan.mode = 0;
+  g->grid = grid;
+  g->max_ks = max_ks;
+  static bool configured = false;
+  if (!configured) {
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(gemv_group_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kGSmem));
+    configured = true;
+  }
+  *out = g;
+  return QIGEN_OK;
+}
+
+static int g_group_mode = 0;
+extern "C" int qigen_debug_group_mode(int mode) {
+  g_group_mode = mode;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_gemv_group_run(const qigen_gemv_group* g, void* stream) {
+  QIGEN_CHECK_ARG(g, QIGEN_ERR_ARG, "null group");
+  GPlan plan = g->plan;
+  plan.mode = g_group_mode;
+  cudaLaunchAttribute pa;
+  pa.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pa.val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t pc = {};
+  pc.gridDim = dim3((unsigned)((g->max_ks * 64 + 255) / 256), (unsigned)g->plan.count, 1);
+  pc.blockDim = dim3(256, 1, 1);
+  pc.stream = (cudaStream_t)stream;
+  pc.attrs = &pa;
+  pc.numAttrs = 1;
+  QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, group_prep_kernel, plan));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g->grid, 1, 1);
+  cfg.blockDim = dim3((kGWarps + 1) * 32, 1, 1);
+  cfg.dynamicSmemBytes = kGSmem;
+  cfg.stream = (cudaStream_t)stream;
+  cfg.attrs = &pa;
+  cfg.numAttrs = 1;
+  QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, gemv_group_kernel, plan));
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_gemv_group_destroy(qigen_gemv_group* g) {
+  if (!g) return QIGEN_OK;
+  if (g->blob) cudaFree(g->blob);
+  if (g->rec) cudaFree(g->rec);
+  delete g;
+  return QIGEN_OK;
+}

@@ -156,12 +156,15 @@ class PanelWeights:
 
     def gemv(self, x: torch.Tensor, out: torch.Tensor | None = None, *, accumulate: bool = False,
              k_splits: int = 0, prologue: str | None = None, norm_weight: torch.Tensor | None = None,
-             eps: float = 1e-5) -> torch.Tensor:
+             eps: float = 1e-5, x_ready: bool = False) -> torch.Tensor:
         """y[t, :] = f(x[t, :]) @ W for t < tokens; x: CUDA [tokens, n] or [n].
 
         ``prologue`` fuses the producer-side glue into the GEMV: None (f = id),
         ``"rmsnorm"`` (f = RMSNorm with ``norm_weight``) or ``"swiglu"`` (x holds
-        gate | up, [tokens, 2n]; f = silu(gate) * up)."""
+        gate | up, [tokens, 2n]; f = silu(gate) * up).  ``x_ready`` asserts that
+        x is not the output of the kernel launched just before on this stream
+        (independent GEMVs back to back): the GEMV then overlaps that kernel
+        completely (QIGEN_GEMV_X_READY)."""
         squeeze = x.dim() == 1
         x2 = x.reshape(1, -1) if squeeze else x
         width = 2 * self.n if prologue == "swiglu" else self.n
@@ -173,8 +176,10 @@ class PanelWeights:
             raise ConfigError("rmsnorm prologue needs a float32 CUDA weight of length n")
         if x2.dtype not in _DTYPES:
             x2 = x2.float()
+            x_ready = False  # x is now the conversion kernel's output
         if x2.stride(1) != 1:
             x2 = x2.contiguous()
+            x_ready = False
         T = x2.shape[0]
         if out is None:
             out = torch.empty((T, self.m), dtype=torch.float32, device=x2.device)
@@ -200,10 +205,59 @@ class PanelWeights:
             xs, ys = x2[t0:t1], y2[t0:t1]
             call("qigen_gemv_ex", self.qw.data_ptr(), self.qsz.data_ptr(), self.n, self.m,
                  self.bits, self.group_code, xs.data_ptr(), _DTYPES[xs.dtype], t1 - t0,
-                 xs.stride(0), ys.data_ptr(), ys.stride(0), int(accumulate), int(k_splits), mode,
+                 xs.stride(0), ys.data_ptr(), ys.stride(0),
+                 int(accumulate) | (X_READY if x_ready else 0), int(k_splits), mode,
                  norm_weight.data_ptr() if mode == 1 else None, float(eps), ws.data_ptr(),
                  ws.numel(), st)
         return out.reshape(self.m) if squeeze else out
+
+
+X_READY = 2  # QIGEN_GEMV_X_READY (include/qigen_b200.h)
+
+
+class GemvGroup:
+    """Independent GEMVs y_i = x_i @ W_i run as ONE persistent launch
+    (qigen_gemv_group_*): the replacement for a loop of independent
+    ``qgemv(pm_i, x_i)`` calls (SPEC.md:349-357).  ``entries`` are
+    ``(PanelWeights, x, y)`` with x CUDA [n] / [tokens <= 2, n] and y f32
+    [m] / [tokens, m]; the tensors are referenced, not copied, so later writes
+    to x are seen by the next ``run()``.  ``run()`` is stream-ordered and
+    graph-capturable."""
+
+    def __init__(self, entries):
+        import ctypes
+
+        from ._lib import GemvDesc
+        self._keep = []
+        descs = (GemvDesc * len(entries))()
+        for i, (pw, x, y) in enumerate(entries):
+            x2 = x.reshape(1, -1) if x.dim() == 1 else x
+            y2 = y.reshape(1, -1) if y.dim() == 1 else y
+            if x2.dtype not in _DTYPES or x2.stride(1) != 1 or not x2.is_cuda:
+                raise ConfigError("group x must be a CUDA f32/f16/bf16 tensor with unit stride")
+            if y2.dtype != torch.float32 or y2.stride(1) != 1 or y2.shape != (x2.shape[0], pw.m):
+                raise ConfigError(f"group y must be float32 [{x2.shape[0]}, {pw.m}]")
+            if x2.shape[1] != pw.n:
+                raise ConfigError(f"x has {x2.shape[1]} columns, expected {pw.n}")
+            descs[i] = GemvDesc(pw.qw.data_ptr(), pw.qsz.data_ptr(), pw.n, pw.m, pw.bits,
+                                pw.group_code, x2.data_ptr(), _DTYPES[x2.dtype], x2.shape[0],
+                                x2.stride(0), y2.data_ptr(), y2.stride(0))
+            self._keep += [pw, x, y]
+        h = ctypes.c_void_p()
+        call("qigen_gemv_group_create", len(entries), ctypes.addressof(descs), ctypes.byref(h))
+        self._h = h
+        self.nbytes_algorithmic = sum(pw.nbytes_algorithmic() for pw, _, _ in entries)
+
+    def run(self) -> None:
+        call("qigen_gemv_group_run", self._h, _dev.stream_handle())
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().qigen_gemv_group_destroy(h)
+            except Exception:  # noqa: BLE001
+                pass
 
 
 def exec_layout(pm) -> PanelWeights:
