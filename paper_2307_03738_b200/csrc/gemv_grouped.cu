@@ -37,10 +37,14 @@ namespace qigen {
 constexpr int kGWarps = 16;            // consumer warps per CTA (panels per item)
 constexpr int kGTP = 2;                // tokens in the fragment layout (M <= 2)
 constexpr int kRecDig = 8 * kGTP * 128;  // digit bytes per superstep record
-constexpr int kRecBytes = kRecDig + 8 * kGTP * 8;  // + (xsum, 2^(E-30)) per unit
-constexpr int kGSlot = 4 * 512 + 8 * 128;  // largest weight stage (4-bit, g = 32)
-constexpr int kGDepth = 4;                 // weight stages per consumer warp
-constexpr int kGRecDepth = 8;              // activation records in the CTA ring
+// + per unit and token {2^(E-30) * 2^16, X * 2^(E-30), 2^(E-30), 0}: the flush
+// factors of the even (digits d0 d1) and odd (d2 d3) lanes, one LDS.64 each
+constexpr int kRecBytes = kRecDig + 8 * kGTP * 16;
+constexpr int kGSS = 2;                // supersteps per ring stage
+constexpr int kGSlot = kGSS * (4 * 512 + 8 * 128);  // largest weight stage (4-bit, g = 32)
+constexpr int kGDepth = 2;             // weight stages per consumer warp
+constexpr int kRecSlot = kGSS * kRecBytes;
+constexpr int kGRecDepth = 4;          // activation-record stages in the CTA ring
 
 struct GDesc {
   const uint4* qw;
@@ -99,8 +103,10 @@ __device__ __forceinline__ void group_prep_item(const GPlan& pl, const GDesc& d,
       store_digits((uint32_t*)rec, sl, tk, kGTP, sub, dg);
       if ((it % IPU) == 0) {
         const int uj = (it % 64) / IPU;
-        ((float2*)(rec + kRecDig))[uj * kGTP + tk] =
-            tk < d.M ? make_float2(dg.xsum, dg.scale) : make_float2(0.f, 0.f);
+        // dg.scale is a power of two: both products are exact
+        ((float4*)(rec + kRecDig))[uj * kGTP + tk] =
+            tk < d.M ? make_float4(dg.scale * 65536.f, dg.xsum * dg.scale, dg.scale, 0.f)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
   }
@@ -130,7 +136,9 @@ __device__ __forceinline__ void imma0(int (&c)[4], const uint32_t (&a)[4], uint2
 
 // Accumulate one 256-row superstep of one panel: 8 IMMA steps + unit flushes.
 // w: the lane's weight words; szs: (s, z) of the groups of this superstep;
-// rec: the activation record of this superstep.
+// rec: the activation record of this superstep.  Flush of unit u, row r:
+//   y_r += s_r * (A q_r - z_r B),  q_r the exact digit-pair partial,
+//   (A, B) = (2^(E-30) 2^16, X 2^(E-30)) on even lanes, (2^(E-30), 0) on odd.
 template <int BITS, int GPS>
 __device__ __forceinline__ void group_superstep(const uint4 (&w)[BITS], const float2* szs,
                                                 const unsigned char* rec, float (&yv)[2]) {
@@ -138,10 +146,7 @@ __device__ __forceinline__ void group_superstep(const uint4 (&w)[BITS], const fl
   constexpr int SPU = 8 / UPS;
   const int lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
   const uint2* bs = (const uint2*)rec + (gq >> 2) * 16 + (gq & 3) * 4 + t;
-  const float2* xs = (const float2*)(rec + kRecDig);
-  const float w_lo = (t & 1) ? 1.f : 65536.f;
-  const float w_hi = w_lo * RowScale<BITS>::inv_hi;
-  const bool xon = (t & 1) == 0;
+  const float2* ab = (const float2*)(rec + kRecDig) + (t >> 1) * 2 + (t & 1);
   int acc[2][4];
 #pragma unroll
   for (int sl = 0; sl < 8; ++sl) {
@@ -154,8 +159,7 @@ __device__ __forceinline__ void group_superstep(const uint4 (&w)[BITS], const fl
       const int uj = (sl + 1) / SPU - 1;
       const int gi = GPS >= UPS ? uj : 0;
       const float2 sz0 = szs[gi * 16 + gq], sz1 = szs[gi * 16 + gq + 8];
-      const float2 xv = xs[uj * kGTP + (t >> 1)];
-      const float X = xon ? xv.x : 0.f, sc = xv.y;
+      const float2 f = ab[uj * kGTP * 2];
       constexpr int sh = BITS == 2 ? 4 : 0;  // 2-bit odd steps carry an extra x16
       int c0, c1, c2, c3;
       if (SPU == 1) {  // one step per unit: only its chain holds data
@@ -166,8 +170,8 @@ __device__ __forceinline__ void group_superstep(const uint4 (&w)[BITS], const fl
         c2 = acc[0][2] + (acc[1][2] >> sh); c3 = acc[0][3] + (acc[1][3] >> sh);
       }
       const float q0 = (float)(c0 * 256 + c1), q1 = (float)(c2 * 256 + c3);
-      yv[0] = fmaf(sz0.x * sc, fmaf(-sz0.y, X, q0 * w_lo), yv[0]);
-      yv[1] = fmaf(sz1.x * sc, fmaf(-sz1.y, X, q1 * w_hi), yv[1]);
+      yv[0] = fmaf(sz0.x, fmaf(-sz0.y, f.y, f.x * q0), yv[0]);
+      yv[1] = fmaf(sz1.x, fmaf(-sz1.y, f.y, (f.x * RowScale<BITS>::inv_hi) * q1), yv[1]);
     }
   }
 }
@@ -177,8 +181,8 @@ __device__ __forceinline__ int gcombo(const GDesc& d) { return (d.bits - 2) * 5 
 __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const GPlan pl) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* rring = smem + kGWarps * kGDepth * kGSlot;           // [DD][record]
-  uint64_t* wfull = (uint64_t*)(rring + kGRecDepth * kRecBytes);      // [warp][D]
+  unsigned char* rring = smem + kGWarps * kGDepth * kGSlot;           // [DD][kGSS records]
+  uint64_t* wfull = (uint64_t*)(rring + kGRecDepth * kRecSlot);       // [warp][D]
   uint64_t* rfull = wfull + kGWarps * kGDepth;                        // [DD]
   uint64_t* rempty = rfull + kGRecDepth;
   const int i0 = pl.cta_start[blockIdx.x], i1 = pl.cta_start[blockIdx.x + 1];
@@ -202,13 +206,14 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
       for (int it = i0; it < i1; ++it) {
         const GDesc& d = pl.desc[pl.items[it].d];
         // fields in registers: the asm memory clobbers below would otherwise
-        // force a global reload per record
+        // force a global reload per stage
         const int KS = d.KS;
         const unsigned char* src = pl.rec + (size_t)d.rec0 * kRecBytes;
-        for (int s = 0; s < KS; ++s) {
+        for (int s = 0; s < KS; s += kGSS) {
+          const uint32_t bytes = (uint32_t)(min(kGSS, KS - s) * kRecBytes);
           mbar_wait(&rempty[slot], ph ^ 1u);
-          mbar_expect_tx(&rfull[slot], kRecBytes);
-          bulk_g2s(rring + slot * kRecBytes, src + (size_t)s * kRecBytes, kRecBytes, &rfull[slot]);
+          mbar_expect_tx(&rfull[slot], bytes);
+          bulk_g2s(rring + slot * kRecSlot, src + (size_t)s * kRecBytes, bytes, &rfull[slot]);
           if (++slot == kGRecDepth) {
             slot = 0;
             ph ^= 1u;
@@ -222,12 +227,13 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
   // ---- consumer warp: panel p0 + warp of every item of this CTA ---------------
   unsigned char* ring = smem + warp * kGDepth * kGSlot;
   uint64_t* full = wfull + warp * kGDepth;
-  // Issue cursor (lane 0) over this warp's (item, superstep) stream, skipping
-  // items in which the warp has no panel (ragged last item of a GEMV); the
-  // current item's stream geometry is cached in registers.
-  int ci = i0, cs = 0, issued = 0;
+  // Issue cursor (lane 0) over this warp's stream of stages (kGSS supersteps of
+  // its panel: weights, then the (s, z) of their groups at offset kGSS * wb),
+  // skipping items in which the warp has no panel (ragged last item of a
+  // GEMV); the current item's geometry is cached in registers.
+  int ci = i0, cs = 0, islot = 0;
   int c_ks = 0, c_gps = 0, c_g = 0;
-  uint32_t c_wb = 0, c_zb = 0;
+  uint32_t c_wb = 0;
   const char *c_w = nullptr, *c_z = nullptr;
   auto load_item = [&]() {
     while (ci < i1) {
@@ -239,7 +245,6 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
         c_gps = d.gps;
         c_g = d.g;
         c_wb = d.bits * 512;
-        c_zb = (d.gps > 0 ? d.gps : 1) * 128;
         c_w = (const char*)d.qw + (int64_t)p * d.KS * c_wb;
         c_z = (const char*)(d.qsz + (int64_t)p * d.Gp * 16);
         return;
@@ -247,14 +252,24 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
       ++ci;
     }
   };
-  auto issue_one = [&]() {  // next stage of the stream into slot issued % D
-    const int slot = issued % kGDepth;
-    const int64_t gfirst = c_gps > 0 ? (int64_t)cs * c_gps : (c_g ? (int64_t)cs * kSuper / c_g : 0);
-    mbar_expect_tx(&full[slot], c_wb + c_zb);
-    bulk_g2s(ring + slot * kGSlot, c_w + (int64_t)cs * c_wb, c_wb, &full[slot]);
-    bulk_g2s(ring + slot * kGSlot + c_wb, c_z + gfirst * 128, c_zb, &full[slot]);
-    ++issued;
-    if (++cs == c_ks) {
+  auto issue_one = [&]() {  // next stage of the stream into slot islot
+    const int nss = min(kGSS, c_ks - cs);
+    unsigned char* dst = ring + islot * kGSlot;
+    uint64_t* bar = &full[islot];
+    const uint32_t zb = (uint32_t)((c_gps > 0 ? nss * c_gps : nss) * 128);
+    mbar_expect_tx(bar, nss * c_wb + zb);
+    bulk_g2s(dst, c_w + (int64_t)cs * c_wb, nss * c_wb, bar);
+    if (c_gps > 0) {
+      bulk_g2s(dst + kGSS * c_wb, c_z + (int64_t)cs * c_gps * 128, zb, bar);
+    } else {  // one group per superstep: the one containing it
+      for (int j = 0; j < nss; ++j) {
+        const int64_t gi = c_g ? (int64_t)(cs + j) * kSuper / c_g : 0;
+        bulk_g2s(dst + kGSS * c_wb + j * 128, c_z + gi * 128, 128, bar);
+      }
+    }
+    if (++islot == kGDepth) islot = 0;
+    cs += nss;
+    if (cs == c_ks) {
       ++ci;
       cs = 0;
       load_item();
@@ -262,11 +277,12 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
   };
   if (lane == 0) {
     load_item();
-    while (ci < i1 && issued < kGDepth) issue_one();
+    for (int i = 0; i < kGDepth && ci < i1; ++i) issue_one();
   }
   __syncwarp();
 
-  int consumed = 0, rn = 0;
+  int wslot = 0, rslot = 0;
+  uint32_t wph = 0, rph = 0;
   bool waited = false;
   for (int it = i0; it < i1; ++it) {
     const GItem itm = pl.items[it];
@@ -275,40 +291,51 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
     const bool active = p < d.P;
     const int combo = gcombo(d);
     const int KS = d.KS;  // registers (see the producer)
+    const int wb = d.bits * 512, zpj = (d.gps > 0 ? d.gps : 1) * 128;
     float yv[2] = {0.f, 0.f};
-    for (int s = 0; s < KS; ++s) {
-      const int rs = rn % kGRecDepth;
-      mbar_wait(&rfull[rs], (uint32_t)(rn / kGRecDepth) & 1u);
+    for (int s = 0; s < KS; s += kGSS) {
+      const int nss = min(kGSS, KS - s);
+      mbar_wait(&rfull[rslot], rph);
       if (active) {
-        const int slot = consumed % kGDepth;
-        mbar_wait(&full[slot], (uint32_t)(consumed / kGDepth) & 1u);
-        const unsigned char* stg = ring + slot * kGSlot;
-        const unsigned char* rec = rring + rs * kRecBytes;
+        mbar_wait(&full[wslot], wph);
+        const unsigned char* stg = ring + wslot * kGSlot;
+        const unsigned char* rec = rring + rslot * kRecSlot;
         if (pl.mode != 1) {
-          switch (combo) {
-#define QG_CASE(B, G)                                                               \
-  case (B - 2) * 5 + G: {                                                           \
-    uint4 w[B];                                                                     \
-    _Pragma("unroll") for (int v = 0; v < B; ++v) w[v] = ((const uint4*)stg)[v * 32 + lane]; \
-    group_superstep<B, G>(w, (const float2*)(stg + B * 512), rec, yv);              \
+          for (int j = 0; j < nss; ++j) {
+            const unsigned char* wj = stg + j * wb;
+            const float2* zj = (const float2*)(stg + kGSS * wb + j * zpj);
+            const unsigned char* rj = rec + j * kRecBytes;
+            switch (combo) {
+#define QG_CASE(B, G)                                                                         \
+  case (B - 2) * 5 + G: {                                                                     \
+    uint4 w[B];                                                                               \
+    _Pragma("unroll") for (int v = 0; v < B; ++v) w[v] = ((const uint4*)wj)[v * 32 + lane];  \
+    group_superstep<B, G>(w, zj, rj, yv);                                                     \
   } break;
-            QG_CASE(2, 0) QG_CASE(2, 1) QG_CASE(2, 2) QG_CASE(2, 4) QG_CASE(2, 8)
-            QG_CASE(3, 0) QG_CASE(3, 1) QG_CASE(3, 2) QG_CASE(3, 4) QG_CASE(3, 8)
-            QG_CASE(4, 0) QG_CASE(4, 1) QG_CASE(4, 2) QG_CASE(4, 4) QG_CASE(4, 8)
+              QG_CASE(2, 0) QG_CASE(2, 1) QG_CASE(2, 2) QG_CASE(2, 4) QG_CASE(2, 8)
+              QG_CASE(3, 0) QG_CASE(3, 1) QG_CASE(3, 2) QG_CASE(3, 4) QG_CASE(3, 8)
+              QG_CASE(4, 0) QG_CASE(4, 1) QG_CASE(4, 2) QG_CASE(4, 4) QG_CASE(4, 8)
 #undef QG_CASE
-            default: break;
+              default: break;
+            }
           }
         }
-        ++consumed;
         __syncwarp();
         if (lane == 0 && ci < i1) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue_one();
         }
+        if (++wslot == kGDepth) {
+          wslot = 0;
+          wph ^= 1u;
+        }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&rempty[rs]);
-      ++rn;
+      if (lane == 0) mbar_arrive(&rempty[rslot]);
+      if (++rslot == kGRecDepth) {
+        rslot = 0;
+        rph ^= 1u;
+      }
     }
     if (active) {
       const int gq = lane >> 2, t = lane & 3;
@@ -328,7 +355,7 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
   }
 }
 
-constexpr int kGSmem = kGWarps * kGDepth * kGSlot + kGRecDepth * kRecBytes +
+constexpr int kGSmem = kGWarps * kGDepth * kGSlot + kGRecDepth * kRecSlot +
                        (kGWarps * kGDepth + 2 * kGRecDepth) * 8;
 
 }  // namespace qigen
@@ -395,8 +422,13 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
     for (int p0 = 0; p0 < d.P; p0 += kGWarps) {
       const int act = std::min(kGWarps, d.P - p0);
       items.push_back({i, p0});
+      // time model per SM: max(stream at ~44 GB/s, issue at ~4.5 instr/ns);
+      // ~110 warp instructions per panel superstep + ~17 per flush unit
       const int zb = (d.gps > 0 ? d.gps : 1) * 128;
-      cost.push_back((double)d.KS * (act * (d.bits * 512 + zb) + kRecBytes));
+      const int ups = d.gps > 2 ? d.gps : 2;
+      const double bytes = (double)d.KS * (act * (d.bits * 512 + zb) + kRecBytes);
+      const double instr = (double)d.KS * act * (110.0 + 17.0 * ups);
+      cost.push_back(std::max(bytes / 44.0, instr / 4.5));
     }
   }
   int dev = 0, sms = 148;
