@@ -15,7 +15,7 @@ from .quant import (CodeMatrix, GroupParams, dequantize, dequantize_matrix, quan
                     quantize_matrix)
 from .packing import (Layout, PackedMatrix, PackError, block_order, extract_codes,
                       lay_out_blocks, morton_index, pack_words, unpack_words)
-from .runtime import (InputSums, PanelWeights, input_sums, memory_report, qgemv,
-                      qgemv_reference)
+from .runtime import (GemvGroup, InputSums, PanelWeights, input_sums, memory_report, qgemv,
+                      qgemv_batch, qgemv_reference)
 
 __version__ = "0.1.0"

@@ -8,19 +8,25 @@
 // §4).  When the GEMVs are independent (the reference runtime's per-matrix
 // qgemv calls of a sweep; the BASELINE configs[1] workload) a
 // persistent schedule hides all of it:
-//   * one CTA per SM, 16 consumer warps + 1 producer warp;
-//   * a work item is one GEMV x 16 panels (256 output columns) x the FULL K
-//     range, so every output column is reduced by exactly one warp in a fixed
-//     order: deterministic, no split-K, no atomics, no cross-CTA traffic;
-//   * items are assigned to CTAs on the host by longest-processing-time-first
-//     greedy on their byte counts (a static, reproducible balance);
-//   * each consumer warp streams its panel of every item of its CTA through its
-//     own ring of TMA bulk-copy stages, issuing ahead ACROSS item boundaries, so
-//     the weight stream never drains between GEMVs;
-//   * the activations of all GEMVs are digitised once by group_prep_kernel into
-//     per-superstep records (digits + unit sums/exponents) which the producer
-//     warp streams through a CTA-shared ring, behind the PDL wait on the prep
-//     kernel (the weight prefetch is issued before it).
+//   * one CTA per SM: 16 consumer warps + 1 activation-record producer warp;
+//   * a work item is one GEMV x 16 panels (256 output columns) x its K range
+//     (the full K by default), so every output column is reduced by one warp
+//     in a fixed order: deterministic, no atomics, no cross-CTA traffic;
+//   * group_prep_kernel digitises the activations of all GEMVs into
+//     per-superstep records (digits + unit flush factors); the grouped kernel
+//     streams its first weight stages meanwhile and waits for it (PDL) before
+//     reading records or claiming items;
+//   * items are ordered by a cost model (bytes vs issue time) and scheduled
+//     greedily: CTA c starts with item c, then claims the next unclaimed item
+//     from a global counter - list scheduling in decreasing-cost order, robust
+//     to the model's errors; the claimer stages the item's geometry in shared
+//     memory, normally a few stages before it is needed;
+//   * each consumer warp streams its panel of every item through its own ring
+//     of TMA bulk-copy stages (2 supersteps of weights + their (s, z)), refilled
+//     by its lane 0 ahead ACROSS item boundaries, so the weight stream never
+//     drains between GEMVs and a slow copy stalls only its own panel;
+//   * the producer warp streams the activation records through a CTA-shared
+//     ring.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -34,6 +40,8 @@
 
 namespace qigen {
 
+extern unsigned long long* g_trace;  // gemv.cu (qigen_debug_trace)
+
 constexpr int kGWarps = 16;            // consumer warps per CTA (panels per item)
 constexpr int kGTP = 2;                // tokens in the fragment layout (M <= 2)
 constexpr int kRecDig = 8 * kGTP * 128;  // digit bytes per superstep record
@@ -45,6 +53,7 @@ constexpr int kGSlot = kGSS * (4 * 512 + 8 * 128);  // largest weight stage (4-b
 constexpr int kGDepth = 2;             // weight stages per consumer warp
 constexpr int kRecSlot = kGSS * kRecBytes;
 constexpr int kGRecDepth = 4;          // activation-record stages in the CTA ring
+constexpr int kMaxSeq = 2048;          // items one CTA may claim (dynamic schedule)
 
 struct GDesc {
   const uint4* qw;
@@ -53,18 +62,24 @@ struct GDesc {
   float* y;
   int64_t ldx, ldy, n, m;
   int KS, P, Gp, g, bits, gps, M, x_dtype;
+  int split;     // 1: K is split in two items whose partials are atomically added to
+                 // a zeroed y (two addends: commutative, so still deterministic)
   int64_t rec0;  // index of this GEMV's first superstep record in the workspace
 };
 struct GItem {
-  int d, p0;
+  int d, p0, k0, k1;  // GEMV, first panel, superstep range
 };
 struct GPlan {
   const GDesc* desc;
   const GItem* items;
-  const int* cta_start;  // [grid + 1]
+  const int* cta_start;  // [grid + 1] (static schedule)
   unsigned char* rec;    // activation records
+  int* counter;          // dynamic schedule: next unclaimed item (re-armed in phase 1)
+  int nitems, first_dyn, dynamic;
+  int64_t total_items;   // activation items (4 rows) of all GEMVs
   int count;
   int mode;              // tuning: 1 = stream only (no compute)
+  unsigned long long* trace;  // optional per-CTA %globaltimer (entry, exit)
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -112,11 +127,19 @@ __device__ __forceinline__ void group_prep_item(const GPlan& pl, const GDesc& d,
   }
 }
 
-// Activation records of every GEMV of the group; grid (ceil(max KS*64/256), count).
+// Activation records of every GEMV of the group; grid (ceil(max KS*64/256),
+// count), launched just before the grouped kernel (which prefetches weights
+// meanwhile and waits for it before reading records or claiming items).
 __global__ void __launch_bounds__(256) group_prep_kernel(const GPlan pl) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
+  // the previous grouped launch has completed: re-arm the dynamic schedule
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && pl.dynamic)
+    *pl.counter = pl.first_dyn;
   const GDesc& d = pl.desc[blockIdx.y];
+  if (d.split)  // the two K halves add into a zeroed y
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < (int64_t)d.M * d.m; i += gridDim.x * 256)
+      d.y[(i / d.m) * d.ldy + i % d.m] = 0.f;
   if ((int)blockIdx.x * 256 >= d.KS * 64) return;
   const int it = blockIdx.x * 256 + threadIdx.x;
   const int U = d.g == 32 ? 32 : d.g == 64 ? 64 : 128;  // exponent unit (rows)
@@ -178,6 +201,72 @@ __device__ __forceinline__ void group_superstep(const uint4 (&w)[BITS], const fl
 
 __device__ __forceinline__ int gcombo(const GDesc& d) { return (d.bits - 2) * 5 + d.gps; }
 
+// Everything a warp needs about one item, staged in shared memory by the
+// thread that claims the item (so no warp stalls on global loads at an item
+// boundary).  Ring of kInfo entries indexed by sequence position.
+struct GInfo {
+  const char* w;            // weights of the item's first panel
+  const char* z;            // (s, z) of the item's first panel
+  float* y;
+  const unsigned char* rec; // the GEMV's first activation record
+  int64_t wstride, zstride, ldy;
+  int p0, k0, k1, P, gps, g, wb, M, m, split, combo;
+};
+constexpr int kInfo = 8;
+
+__device__ __forceinline__ void fill_info(GInfo* inf, const GPlan& pl, int id) {
+  const GItem itm = pl.items[id];
+  const GDesc& d = pl.desc[itm.d];
+  const int wb = d.bits * 512;
+  inf->wstride = (int64_t)d.KS * wb;
+  inf->zstride = (int64_t)d.Gp * 16 * 8;
+  inf->w = (const char*)d.qw + itm.p0 * inf->wstride;
+  inf->z = (const char*)d.qsz + itm.p0 * inf->zstride;
+  inf->y = d.y;
+  inf->rec = pl.rec + (size_t)d.rec0 * kRecBytes;
+  inf->ldy = d.ldy;
+  inf->p0 = itm.p0;
+  inf->k0 = itm.k0;
+  inf->k1 = itm.k1;
+  inf->P = d.P;
+  inf->gps = d.gps;
+  inf->g = d.g;
+  inf->wb = wb;
+  inf->M = d.M;
+  inf->m = (int)d.m;
+  inf->split = d.split;
+  inf->combo = gcombo(d);
+}
+
+// Item k of this CTA's sequence (-1: done); info[k % kInfo] is valid after it
+// returns >= 0.  Static schedule: the host's LPT list.  Dynamic schedule: item
+// 0 is the CTA's static first item (so its weights stream before the PDL
+// wait); later items are claimed from a global counter in decreasing-cost
+// order by whichever thread of the CTA needs them first (normally the record
+// producer, a few stages ahead), which also stages their info.
+__device__ __forceinline__ int seq_get(volatile int* seq, GInfo* info, int k, const GPlan& pl) {
+  if (k >= kMaxSeq) return -1;  // (host guarantees the sequence fits)
+  int v = seq[k];
+  if (v == -2 && atomicCAS((int*)&seq[k], -2, -3) == -2) {
+    if (!pl.dynamic) {
+      const int i = pl.cta_start[blockIdx.x] + k;
+      v = i < pl.cta_start[blockIdx.x + 1] ? i : -1;
+    } else {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // counter re-armed by the prep kernel
+      const int c = atomicAdd(pl.counter, 1);
+      v = c < pl.nitems ? c : -1;
+    }
+    if (v >= 0) fill_info(&info[k % kInfo], pl, v);
+    __threadfence_block();
+    seq[k] = v;
+    return v;
+  }
+  while ((v = seq[k]) < -1) {
+  }
+  __threadfence_block();
+  return v;
+}
+
 __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const GPlan pl) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -185,8 +274,16 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
   uint64_t* wfull = (uint64_t*)(rring + kGRecDepth * kRecSlot);       // [warp][D]
   uint64_t* rfull = wfull + kGWarps * kGDepth;                        // [DD]
   uint64_t* rempty = rfull + kGRecDepth;
-  const int i0 = pl.cta_start[blockIdx.x], i1 = pl.cta_start[blockIdx.x + 1];
+  GInfo* info = (GInfo*)(rempty + kGRecDepth);                        // [kInfo]
+  volatile int* seq = (volatile int*)(info + kInfo);                  // [kMaxSeq]
   asm volatile("griddepcontrol.launch_dependents;");
+  if (pl.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    pl.trace[blockIdx.x * 4] = t;
+  }
+  for (int i = threadIdx.x; i < kMaxSeq; i += blockDim.x) seq[i] = -2;
+  __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 0; i < kGWarps * kGDepth; ++i) mbar_init(&wfull[i], 1);
     for (int i = 0; i < kGRecDepth; ++i) {
@@ -194,66 +291,50 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
       mbar_init(&rempty[i], kGWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // item 0: static (dynamic schedule: item blockIdx.x), needs no PDL wait
+    const int i0 = pl.dynamic ? (int)blockIdx.x : pl.cta_start[blockIdx.x];
+    const bool any = pl.dynamic ? true : i0 < pl.cta_start[blockIdx.x + 1];
+    if (any) fill_info(&info[0], pl, i0);
+    seq[0] = any ? i0 : -1;
   }
   __syncthreads();
 
-  if (warp == kGWarps) {
-    // ---- activation-record producer (after the PDL wait on the prep kernel)
-    if (lane == 0) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      int slot = 0;
-      uint32_t ph = 0;
-      for (int it = i0; it < i1; ++it) {
-        const GDesc& d = pl.desc[pl.items[it].d];
-        // fields in registers: the asm memory clobbers below would otherwise
-        // force a global reload per stage
-        const int KS = d.KS;
-        const unsigned char* src = pl.rec + (size_t)d.rec0 * kRecBytes;
-        for (int s = 0; s < KS; s += kGSS) {
-          const uint32_t bytes = (uint32_t)(min(kGSS, KS - s) * kRecBytes);
-          mbar_wait(&rempty[slot], ph ^ 1u);
-          mbar_expect_tx(&rfull[slot], bytes);
-          bulk_g2s(rring + slot * kRecSlot, src + (size_t)s * kRecBytes, bytes, &rfull[slot]);
-          if (++slot == kGRecDepth) {
-            slot = 0;
-            ph ^= 1u;
-          }
-        }
-      }
-    }
-    return;
-  }
-
-  // ---- consumer warp: panel p0 + warp of every item of this CTA ---------------
+  // ---- weight prefetch of item 0 (independent of every other kernel) --------
   unsigned char* ring = smem + warp * kGDepth * kGSlot;
   uint64_t* full = wfull + warp * kGDepth;
   // Issue cursor (lane 0) over this warp's stream of stages (kGSS supersteps of
   // its panel: weights, then the (s, z) of their groups at offset kGSS * wb),
   // skipping items in which the warp has no panel (ragged last item of a
   // GEMV); the current item's geometry is cached in registers.
-  int ci = i0, cs = 0, islot = 0;
-  int c_ks = 0, c_gps = 0, c_g = 0;
+  int ck = 0, cs = 0, islot = 0;  // cursor: sequence index, superstep, ring slot
+  bool cdone = false;
+  int c_k1 = 0, c_gps = 0, c_g = 0;
   uint32_t c_wb = 0;
   const char *c_w = nullptr, *c_z = nullptr;
   auto load_item = [&]() {
-    while (ci < i1) {
-      const GItem itm = pl.items[ci];
-      const GDesc& d = pl.desc[itm.d];
-      const int p = itm.p0 + warp;
-      if (p < d.P) {
-        c_ks = d.KS;
-        c_gps = d.gps;
-        c_g = d.g;
-        c_wb = d.bits * 512;
-        c_w = (const char*)d.qw + (int64_t)p * d.KS * c_wb;
-        c_z = (const char*)(d.qsz + (int64_t)p * d.Gp * 16);
+    for (;; ++ck) {
+      if (seq_get(seq, info, ck, pl) < 0) {
+        cdone = true;
         return;
       }
-      ++ci;
+      const GInfo& f = info[ck % kInfo];
+      if (f.p0 + warp < f.P) {
+        c_k1 = f.k1;
+        cs = f.k0;
+        c_gps = f.gps;
+        c_g = f.g;
+        c_wb = f.wb;
+        c_w = f.w + warp * f.wstride;
+        c_z = f.z + warp * f.zstride;
+        return;
+      }
     }
   };
-  auto issue_one = [&]() {  // next stage of the stream into slot islot
-    const int nss = min(kGSS, c_ks - cs);
+  // next stage of the stream into slot islot; false at the end of an item
+  // when `advance` is off (the first ring fill stays inside item 0: claiming a
+  // later item waits for the prep kernel)
+  auto issue_one = [&](bool advance) {
+    const int nss = min(kGSS, c_k1 - cs);
     unsigned char* dst = ring + islot * kGSlot;
     uint64_t* bar = &full[islot];
     const uint32_t zb = (uint32_t)((c_gps > 0 ? nss * c_gps : nss) * 128);
@@ -269,32 +350,95 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
     }
     if (++islot == kGDepth) islot = 0;
     cs += nss;
-    if (cs == c_ks) {
-      ++ci;
-      cs = 0;
+    if (cs == c_k1) {
+      ++ck;
+      if (!advance) return false;
       load_item();
     }
+    return true;
   };
-  if (lane == 0) {
+  bool pend = false;  // the cursor stopped at the end of item 0: advance later
+  int npre = 0;       // stages issued before the barrier
+  if (warp < kGWarps && lane == 0) {
+    if (seq[0] >= 0 && info[0].p0 + warp < info[0].P) {
+      load_item();  // item 0 (staged by thread 0, no claim)
+      while (npre < kGDepth) {
+        ++npre;
+        if (!issue_one(false)) {
+          pend = true;
+          break;
+        }
+      }
+    } else {
+      pend = true;  // no panel in item 0: start from item 1 after the barrier
+      ck = 1;
+    }
+  }
+
+  if (warp == kGWarps) {
+    // ---- activation-record producer (after the PDL wait on the prep kernel)
+    if (lane == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int k = 0;; ++k) {
+        if (seq_get(seq, info, k, pl) < 0) break;
+        const GInfo& f = info[k % kInfo];
+        // fields in registers: the asm memory clobbers below would otherwise
+        // force a reload per stage
+        const int K1 = f.k1;
+        const unsigned char* src = f.rec;
+        bool claimed = false;
+        for (int s = f.k0; s < K1; s += kGSS) {
+          // claim (and stage) the next item a few stages before the issue
+          // cursors need it, hiding the global atomic's latency
+          if (!claimed && s + 3 * kGSS >= K1) {
+            seq_get(seq, info, k + 1, pl);
+            claimed = true;
+          }
+          const uint32_t bytes = (uint32_t)(min(kGSS, K1 - s) * kRecBytes);
+          mbar_wait(&rempty[slot], ph ^ 1u);
+          mbar_expect_tx(&rfull[slot], bytes);
+          bulk_g2s(rring + slot * kRecSlot, src + (size_t)s * kRecBytes, bytes, &rfull[slot]);
+          if (++slot == kGRecDepth) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warp: panel p0 + warp of every item of this CTA ---------------
+  if (lane == 0 && pend) {  // top the ring up from the items after item 0
+    // (a claim waits on the prep kernel; the rest of the CTA is not held)
     load_item();
-    for (int i = 0; i < kGDepth && ci < i1; ++i) issue_one();
+    for (; npre < kGDepth && !cdone; ++npre) issue_one(true);
   }
   __syncwarp();
 
   int wslot = 0, rslot = 0;
   uint32_t wph = 0, rph = 0;
   bool waited = false;
-  for (int it = i0; it < i1; ++it) {
-    const GItem itm = pl.items[it];
-    const GDesc& d = pl.desc[itm.d];
-    const int p = itm.p0 + warp;
-    const bool active = p < d.P;
-    const int combo = gcombo(d);
-    const int KS = d.KS;  // registers (see the producer)
-    const int wb = d.bits * 512, zpj = (d.gps > 0 ? d.gps : 1) * 128;
+  for (int k = 0;; ++k) {
+    int it = 0;
+    if (lane == 0) it = seq_get(seq, info, k, pl);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it < 0) break;
+    __threadfence_block();
+    const GInfo& f = info[k % kInfo];
+    const int p = f.p0 + warp;
+    const bool active = p < f.P;
+    const int combo = f.combo;
+    const int K0 = f.k0, K1 = f.k1;  // registers (see the producer)
+    const int wb = f.wb, zpj = (f.gps > 0 ? f.gps : 1) * 128;
+    float* const yg = f.y;
+    const int64_t ldy = f.ldy;
+    const int M = f.M, m = f.m, split = f.split;
     float yv[2] = {0.f, 0.f};
-    for (int s = 0; s < KS; s += kGSS) {
-      const int nss = min(kGSS, KS - s);
+    for (int s = K0; s < K1; s += kGSS) {
+      const int nss = min(kGSS, K1 - s);
       mbar_wait(&rfull[rslot], rph);
       if (active) {
         mbar_wait(&full[wslot], wph);
@@ -321,9 +465,9 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
           }
         }
         __syncwarp();
-        if (lane == 0 && ci < i1) {
+        if (lane == 0 && !cdone) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_one();
+          issue_one(true);
         }
         if (++wslot == kGDepth) {
           wslot = 0;
@@ -346,21 +490,35 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
         asm volatile("griddepcontrol.wait;" ::: "memory");
         waited = true;
       }
-      if ((t & 1) == 0 && tk < d.M) {
+      if ((t & 1) == 0 && tk < M) {
         const int64_t c0 = (int64_t)p * 16 + gq;
-        if (c0 < d.m) d.y[tk * d.ldy + c0] = v0;
-        if (c0 + 8 < d.m) d.y[tk * d.ldy + c0 + 8] = v1;
+        float* yr = yg + tk * ldy;
+        if (split) {
+          if (c0 < m) atomicAdd(yr + c0, v0);
+          if (c0 + 8 < m) atomicAdd(yr + c0 + 8, v1);
+        } else {
+          if (c0 < m) yr[c0] = v0;
+          if (c0 + 8 < m) yr[c0 + 8] = v1;
+        }
       }
     }
+  }
+  if (pl.trace && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&pl.trace[blockIdx.x * 4 + 3], t);
   }
 }
 
 constexpr int kGSmem = kGWarps * kGDepth * kGSlot + kGRecDepth * kRecSlot +
-                       (kGWarps * kGDepth + 2 * kGRecDepth) * 8;
+                       (kGWarps * kGDepth + 2 * kGRecDepth) * 8 + kInfo * sizeof(GInfo) +
+                       kMaxSeq * 4;
 
 }  // namespace qigen
 
 using namespace qigen;
+
+static int g_group_mode = 0;  // tuning: 1 stream only; 16 (at create) split K in two
 
 struct qigen_gemv_group {
   void* blob = nullptr;  // device: descs | items | cta_start
@@ -410,24 +568,31 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
             : e.group_size == 256 ? 1 : 0;
     d.M = (int)e.tokens;
     d.x_dtype = e.x_dtype;
+    // (tuning) split K in two halves when each keeps >= 4 supersteps: halves
+    // the item size and so the greedy schedule's tail, but costs more per-item
+    // overhead than it saves on the configs[1] sweep (measured), so it is off
+    d.split = (d.KS >= 8 && (g_group_mode & 16)) ? 1 : 0;
     d.rec0 = recs;
     recs += d.KS;
     max_ks = std::max(max_ks, d.KS);
   }
-  // items (GEMV x 16 panels x full K) and their stream bytes
+  // items (GEMV x 16 panels x K range) and their cost
   std::vector<GItem> items;
   std::vector<double> cost;
   for (int i = 0; i < count; ++i) {
     const GDesc& d = ds[i];
-    for (int p0 = 0; p0 < d.P; p0 += kGWarps) {
+    const int halves = d.split ? 2 : 1;
+    for (int p0 = 0; p0 < d.P; p0 += kGWarps)
+    for (int hf = 0; hf < halves; ++hf) {
       const int act = std::min(kGWarps, d.P - p0);
-      items.push_back({i, p0});
+      const int k0 = hf * (d.KS / 2), k1 = halves == 1 || hf == 1 ? d.KS : d.KS / 2;
+      items.push_back({i, p0, k0, k1});
       // time model per SM: max(stream at ~44 GB/s, issue at ~4.5 instr/ns);
       // ~110 warp instructions per panel superstep + ~17 per flush unit
       const int zb = (d.gps > 0 ? d.gps : 1) * 128;
       const int ups = d.gps > 2 ? d.gps : 2;
-      const double bytes = (double)d.KS * (act * (d.bits * 512 + zb) + kRecBytes);
-      const double instr = (double)d.KS * act * (110.0 + 17.0 * ups);
+      const double bytes = (double)(k1 - k0) * (act * (d.bits * 512 + zb) + kRecBytes);
+      const double instr = (double)(k1 - k0) * act * (110.0 + 17.0 * ups);
       cost.push_back(std::max(bytes / 44.0, instr / 4.5));
     }
   }
@@ -449,19 +614,32 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
     per[l.second].push_back(i);
     heap.push({l.first + cost[i], l.second});
   }
+  // Dynamic schedule (default): items in decreasing-cost order, CTA c starts
+  // with item c and then claims the next unclaimed one (greedy list
+  // scheduling, which absorbs the model's errors).  Static LPT lists when a
+  // CTA's claim sequence could overflow its shared-memory table.
+  const bool dynamic = (int)items.size() - grid < kMaxSeq;
+  QIGEN_CHECK_ARG(dynamic || (int)items.size() / grid + 2 < kMaxSeq, QIGEN_ERR_UNSUPPORTED,
+                  "grouped GEMV: too many work items (%d)", (int)items.size());
   std::vector<GItem> flat;
   std::vector<int> start(grid + 1, 0);
-  for (int c = 0; c < grid; ++c) {
-    start[c] = (int)flat.size();
-    for (int i : per[c]) flat.push_back(items[i]);
+  if (dynamic) {
+    for (int i : order) flat.push_back(items[i]);
+    for (int c = 0; c <= grid; ++c) start[c] = c;
+  } else {
+    for (int c = 0; c < grid; ++c) {
+      start[c] = (int)flat.size();
+      for (int i : per[c]) flat.push_back(items[i]);
+    }
+    start[grid] = (int)flat.size();
   }
-  start[grid] = (int)flat.size();
 
   auto* g = new qigen_gemv_group();
   const size_t db = ds.size() * sizeof(GDesc), ib = flat.size() * sizeof(GItem),
                sb = start.size() * sizeof(int);
   const size_t ib_off = (db + 255) / 256 * 256, sb_off = ib_off + (ib + 255) / 256 * 256;
-  cudaError_t e1 = cudaMalloc(&g->blob, sb_off + sb);
+  const size_t cnt_off = sb_off + (sb + 255) / 256 * 256;
+  cudaError_t e1 = cudaMalloc(&g->blob, cnt_off + 256);
   cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc((void**)&g->rec, (size_t)recs * kRecBytes) : e1;
   if (e2 != cudaSuccess) {
     if (g->blob) cudaFree(g->blob);
@@ -472,12 +650,20 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
   QIGEN_CUDA_RET(cudaMemcpy(b, ds.data(), db, cudaMemcpyHostToDevice));
   QIGEN_CUDA_RET(cudaMemcpy(b + ib_off, flat.data(), ib, cudaMemcpyHostToDevice));
   QIGEN_CUDA_RET(cudaMemcpy(b + sb_off, start.data(), sb, cudaMemcpyHostToDevice));
+  QIGEN_CUDA_RET(cudaMemset(b + cnt_off, 0, 256));
+  QIGEN_CUDA_RET(cudaMemcpy(b + cnt_off, &grid, sizeof(int), cudaMemcpyHostToDevice));
   g->plan.desc = (const GDesc*)b;
   g->plan.items = (const GItem*)(b + ib_off);
   g->plan.cta_start = (const int*)(b + sb_off);
   g->plan.rec = g->rec;
+  g->plan.counter = (int*)(b + cnt_off);
+  g->plan.nitems = (int)flat.size();
+  g->plan.first_dyn = grid;
+  g->plan.dynamic = dynamic ? 1 : 0;
+  g->plan.total_items = recs * 64;
   g->plan.count = count;
   g->plan.mode = 0;
+  g->plan.trace = nullptr;
   g->grid = grid;
   g->max_ks = max_ks;
   static bool configured = false;
@@ -490,7 +676,6 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
   return QIGEN_OK;
 }
 
-static int g_group_mode = 0;
 extern "C" int qigen_debug_group_mode(int mode) {
   g_group_mode = mode;
   return QIGEN_OK;
@@ -499,7 +684,8 @@ extern "C" int qigen_debug_group_mode(int mode) {
 extern "C" int qigen_gemv_group_run(const qigen_gemv_group* g, void* stream) {
   QIGEN_CHECK_ARG(g, QIGEN_ERR_ARG, "null group");
   GPlan plan = g->plan;
-  plan.mode = g_group_mode;
+  plan.mode = g_group_mode & 15;
+  plan.trace = g_trace;
   cudaLaunchAttribute pa;
   pa.id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pa.val.programmaticStreamSerializationAllowed = 1;

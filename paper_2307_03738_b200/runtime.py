@@ -319,6 +319,60 @@ def qgemv(pm, x, sums=None, threads=None, *, out=None, accumulate: bool = False)
     return y
 
 
+class _Batch:
+    """Device staging + grouped plan for one list of PackedMatrix objects."""
+
+    def __init__(self, pms, dev):
+        self.pms = list(pms)  # keeps the objects (and their ids) alive
+        self.pws = [exec_layout(pm) for pm in self.pms]
+        self.koff = np.cumsum([0] + [pw.n for pw in self.pws])
+        self.noff = np.cumsum([0] + [pw.m for pw in self.pws])
+        self.x = torch.zeros(int(self.koff[-1]), device=dev)
+        self.y = torch.zeros(int(self.noff[-1]), device=dev)
+        self.xh = torch.zeros(int(self.koff[-1])).pin_memory()
+        self.yh = torch.zeros(int(self.noff[-1])).pin_memory()
+        self.group = GemvGroup([(pw, self.x[self.koff[i]:self.koff[i + 1]],
+                                 self.y[self.noff[i]:self.noff[i + 1]])
+                                for i, pw in enumerate(self.pws)])
+
+
+_BATCHES: dict = {}
+
+
+def qgemv_batch(pms, xs):
+    """Independent ``qgemv(pm_i, x_i)`` calls for a list of
+    matrices, as ONE grouped GPU launch (``GemvGroup``).  ``xs``: per matrix an
+    [n_i] activation vector (numpy / CPU tensor, or CUDA f32 tensor).  Host
+    inputs are staged through one pinned buffer (one H2D and one D2H copy per
+    call) and numpy results are returned; device inputs give CUDA tensors.
+    The grouped plan and staging buffers are cached per matrix list."""
+    if len(pms) != len(xs) or not pms:
+        raise ConfigError("qgemv_batch needs one activation vector per matrix")
+    dev = _dev.require_cuda()
+    key = tuple(id(pm) for pm in pms)
+    b = _BATCHES.get(key)
+    if b is None or any(p is not q for p, q in zip(b.pms, pms)):
+        b = _BATCHES[key] = _Batch(pms, dev)
+    host = all(_dev.is_host(x) for x in xs)
+    for i, (pw, x) in enumerate(zip(b.pws, xs)):
+        if tuple(np.shape(x)) != (pw.n,):
+            raise ConfigError(f"x[{i}] has shape {tuple(np.shape(x))}, expected [{pw.n}]")
+        if host:
+            xa = x.numpy() if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float32)
+            b.xh[b.koff[i]:b.koff[i + 1]].numpy()[:] = xa
+        else:
+            b.x[b.koff[i]:b.koff[i + 1]].copy_(x)
+    if host:
+        b.x.copy_(b.xh, non_blocking=True)
+    b.group.run()
+    if host:
+        b.yh.copy_(b.y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        yh = b.yh.numpy()
+        return [yh[b.noff[i]:b.noff[i + 1]].copy() for i in range(len(pms))]
+    return [b.y[b.noff[i]:b.noff[i + 1]].clone() for i in range(len(pms))]
+
+
 def qgemv_reference(pm, x):
     """the unfactored dense oracle, on the GPU — full
     dequantization (quant.py:130-138) then an fp64 matrix product."""

@@ -379,3 +379,100 @@ def test_cfg2_shapes_tensor_core(q):
         Y = pw.gemv(X).double()
         ref = X.double() @ wd
         assert ((Y - ref).abs().max() / (1 + ref.abs().max())).item() <= TOL_TC
+
+
+# --- grouped GEMV (independent GEMVs in one persistent launch) ----------------
+
+def _group_cases(q, specs, seed=0, dtype=torch.float32, tokens=1):
+    from paper_2307_03738_b200.runtime import GemvGroup
+    entries, refs = [], []
+    for i, (K, N, bits, g) in enumerate(specs):
+        cm, codes, s, z, rng = _case(q, K, N, bits, g, seed=seed + i)
+        pw = q.PanelWeights.from_codes(cm)
+        X = torch.from_numpy(rng.normal(0, 1, (tokens, K)).astype(np.float32)).to(dtype)
+        y = torch.full((tokens, N), float("nan"), device="cuda")
+        entries.append((pw, X.cuda(), y))
+        refs.append([orc.qgemv_reference(codes, s, z, X[t].float().numpy()) for t in range(tokens)])
+    return GemvGroup(entries), entries, refs
+
+
+def test_group_gemv_sweep_vs_oracle(q):
+    """BASELINE configs[1] mix (all b x g, the three shapes) in one launch."""
+    specs = [(K, N, b, g) for (K, N) in [(4096, 4096), (4096, 11008), (11008, 4096)]
+             for b in (2, 3, 4) for g in (32, 64, 128, None)]
+    grp, entries, refs = _group_cases(q, specs)
+    grp.run()
+    torch.cuda.synchronize()
+    for (pw, x, y), r, spec in zip(entries, refs, specs):
+        assert rel_err(y[0].cpu().numpy(), r[0]) <= TOL, spec
+
+
+def test_group_gemv_ragged_and_long_groups(q):
+    """Ragged K/N (padding panels, partial stages), g = 256 / 512 / 768 / full
+    column (one (s, z) group per superstep), 2 tokens, repeat runs identical."""
+    specs = [(544, 1000, 4, 32), (288, 40, 3, None), (1024, 17, 2, 64), (768, 300, 4, 256),
+             (1536, 520, 3, 512), (2304, 64, 4, 768), (4352, 4000, 2, 128), (96, 24, 4, None)]
+    grp, entries, refs = _group_cases(q, specs, seed=11, tokens=2)
+    grp.run()
+    torch.cuda.synchronize()
+    first = [y.clone() for _, _, y in entries]
+    for (pw, x, y), r, spec in zip(entries, refs, specs):
+        for t in range(2):
+            assert rel_err(y[t].cpu().numpy(), r[t]) <= TOL, (spec, t)
+    grp.run()
+    torch.cuda.synchronize()
+    for (_, _, y), f in zip(entries, first):
+        assert torch.equal(y, f)  # deterministic
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_group_gemv_half_activations(q, dtype):
+    specs = [(4096, 1024, 4, 128), (2048, 512, 3, 64), (1024, 2048, 2, 32)]
+    grp, entries, refs = _group_cases(q, specs, seed=5, dtype=dtype)
+    grp.run()
+    torch.cuda.synchronize()
+    for (pw, x, y), r, spec in zip(entries, refs, specs):
+        assert rel_err(y[0].cpu().numpy(), r[0]) <= TOL_HALF, spec
+
+
+def test_group_gemv_matches_single_gemv_and_sees_new_inputs(q):
+    """Grouped == per-GEMV kernel to f32 rounding; x is referenced, so a
+    rewrite of x changes the next run; graph capture works."""
+    specs = [(4096, 4096, 4, 128), (11008, 4096, 3, 64)]
+    grp, entries, refs = _group_cases(q, specs, seed=21)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        grp.run()
+        s.synchronize()
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph, stream=s):
+            grp.run()
+    for pw, x, y in entries:
+        x.mul_(-2.0)
+    gph.replay()
+    torch.cuda.synchronize()
+    for pw, x, y in entries:
+        ys = pw.gemv(x)
+        assert rel_err(y.cpu().numpy(), ys.cpu().numpy()) <= 2e-6
+
+
+def test_group_gemv_rejects_bad_input(q):
+    from paper_2307_03738_b200.runtime import GemvGroup
+    cm, *_ = _case(q, 512, 64, 4, 16)
+    pw = q.PanelWeights.from_codes(cm)
+    with pytest.raises(Exception):
+        GemvGroup([(pw, torch.zeros(512, device="cuda"), torch.zeros(64, device="cuda"))])
+
+
+def test_qgemv_batch_public_api(q):
+    """qgemv_batch over reference-format PackedMatrix objects, host in/out."""
+    pms, xs, refs = [], [], []
+    for i, (K, N, b, g) in enumerate([(1024, 512, 4, 128), (2048, 300, 3, 32), (512, 1024, 2, None)]):
+        cm, codes, s, z, rng = _case(q, K, N, b, g, seed=40 + i)
+        pms.append(q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N))))
+        xs.append(rng.normal(0, 1, K).astype(np.float32))
+        refs.append(orc.qgemv_reference(codes, s, z, xs[-1]))
+    for _ in range(2):  # second call reuses the cached plan
+        ys = q.qgemv_batch(pms, xs)
+        for y, r in zip(ys, refs):
+            assert rel_err(y, r) <= TOL

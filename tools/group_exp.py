@@ -17,7 +17,11 @@ for i, (b, g, (K, N)) in enumerate(SWEEP):
     x = torch.randn(K, device=dev)
     pws.append(pw); xs.append(x); ys.append(torch.zeros(N, device=dev))
     yref.append(pw.gemv(x))
+import os
+from paper_2307_03738_b200 import _lib as _L
+_L.lib().qigen_debug_group_mode(int(os.environ.get("GMODE", "0")))
 grp = GemvGroup(list(zip(pws, xs, ys)))
+_L.lib().qigen_debug_group_mode(0)
 grp.run(); torch.cuda.synchronize()
 worst = 0.0
 for (b, g, shp), y, r in zip(SWEEP, ys, yref):
