@@ -331,6 +331,7 @@ class _Batch:
         self.y = torch.zeros(int(self.noff[-1]), device=dev)
         self.xh = torch.zeros(int(self.koff[-1])).pin_memory()
         self.yh = torch.zeros(int(self.noff[-1])).pin_memory()
+        self.xh_np, self.yh_np = self.xh.numpy(), self.yh.numpy()
         self.group = GemvGroup([(pw, self.x[self.koff[i]:self.koff[i + 1]],
                                  self.y[self.noff[i]:self.noff[i + 1]])
                                 for i, pw in enumerate(self.pws)])
@@ -355,22 +356,22 @@ def qgemv_batch(pms, xs):
         b = _BATCHES[key] = _Batch(pms, dev)
     host = all(_dev.is_host(x) for x in xs)
     for i, (pw, x) in enumerate(zip(b.pws, xs)):
-        if tuple(np.shape(x)) != (pw.n,):
-            raise ConfigError(f"x[{i}] has shape {tuple(np.shape(x))}, expected [{pw.n}]")
-        if host:
-            xa = x.numpy() if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float32)
-            b.xh[b.koff[i]:b.koff[i + 1]].numpy()[:] = xa
-        else:
-            b.x[b.koff[i]:b.koff[i + 1]].copy_(x)
+        shp = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
+        if shp != (pw.n,):
+            raise ConfigError(f"x[{i}] has shape {shp}, expected [{pw.n}]")
     if host:
+        # one host-side gather into the pinned staging buffer, one H2D copy
+        np.concatenate([x.numpy() if isinstance(x, torch.Tensor) else x for x in xs],
+                       out=b.xh_np, casting="same_kind")
         b.x.copy_(b.xh, non_blocking=True)
+    else:
+        torch.cat([x.reshape(-1).float() for x in xs], out=b.x)
     b.group.run()
     if host:
         b.yh.copy_(b.y, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        yh = b.yh.numpy()
-        return [yh[b.noff[i]:b.noff[i + 1]].copy() for i in range(len(pms))]
-    return [b.y[b.noff[i]:b.noff[i + 1]].clone() for i in range(len(pms))]
+        return np.split(b.yh_np.copy(), b.noff[1:-1])
+    return list(torch.split(b.y.clone(), [pw.m for pw in b.pws]))
 
 
 def qgemv_reference(pm, x):
