@@ -171,6 +171,22 @@ int qigen_rope_kv(const float* qkv, int64_t batch, int64_t heads, int64_t head_d
 int qigen_rmsnorm_f16(const float* h, const float* w, int64_t rows, int64_t d, float eps,
                       void* out, void* stream);
 
+/* Fused decode attention for one new token per sequence (flash-decoding split
+ * over positions): RoPE on q and the new k at `pos` (cos_pos/sin_pos: [hd/2]),
+ * append of k and v to the f16 caches [batch, heads, ctx, hd], softmax(q K^T *
+ * scale) V over positions 0..pos, out f32 [batch, heads * hd].  head_dim 64 or
+ * 128.  workspace: >= qigen_attn_decode_workspace_size bytes, zero-filled once
+ * before first use (the kernel leaves it reusable).  Launched with programmatic
+ * dependent launch: the cached K/V rows stream before the wait on the kernel
+ * that produced qkv.  Replaces the torch SDPA + RoPE glue of the decode driver
+ * (no reference counterpart: SPEC.md:13,384). */
+int64_t qigen_attn_decode_workspace_size(int64_t batch, int64_t heads, int64_t head_dim,
+                                         int64_t ctx);
+int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
+                      const float* cos_pos, const float* sin_pos, void* k_cache, void* v_cache,
+                      int64_t ctx, int64_t pos, float scale, float* out, void* workspace,
+                      int64_t workspace_bytes, void* stream);
+
 /* Small-batch quantized GEMM on the tcgen05 tensor cores (north_star (c)):
  * weights dequantized to fp16 (w = s (c - z)) in shared memory, activations
  * converted to fp16, f32 accumulation in TMEM.  4-bit, group 32..256 (dividing

@@ -63,6 +63,9 @@ SIGNATURES = {
     "qigen_gemv_group_destroy": (_I32, [_P]),
     "qigen_rope_kv": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "qigen_rmsnorm_f16": (_I32, [_P, _P, _I64, _I64, ctypes.c_float, _P, _P]),
+    "qigen_attn_decode_workspace_size": (_I64, [_I64, _I64, _I64, _I64]),
+    "qigen_attn_decode": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
+                                 ctypes.c_float, _P, _P, _I64, _P]),
     "qigen_gemm_tc_workspace_size": (_I64, [_I64, _I64]),
     "qigen_gemm_tc": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64, _I32,
                              _I32, _P, _I64, _P]),

@@ -6,6 +6,7 @@
 #include <cuda_fp16.h>
 
 #include "common.cuh"
+#include "gemv_common.cuh"
 
 namespace qigen {
 
@@ -70,9 +71,199 @@ __global__ void __launch_bounds__(1024) rmsnorm_f16_kernel(const float* __restri
     out[(size_t)blockIdx.x * d + k] = __float2half_rn(row[k] * inv * w[k]);
 }
 
+// ---- fused decode attention ---------------------------------------------------
+// One new token per sequence attends over its KV cache (flash-decoding split
+// over positions).  Per CTA: one (sequence, head) and a chunk of kAttnChunk
+// positions.  The chunk's cached K/V rows (written by earlier decode steps, not
+// by the preceding kernel) are bulk-copied into shared memory BEFORE the PDL
+// wait, so they stream while the QKV GEMV finishes; after the wait the CTA
+// applies RoPE to q (and, in the chunk holding `pos`, to the new k, appending
+// k/v to the cache), computes its partial softmax state, and the last CTA of
+// the head combines the partials in split order (deterministic).
+constexpr int kAttnChunk = 64;
+
+struct AttnArgs {
+  const float* qkv;  // [B, 3, H, HD] f32 (the fused QKV GEMV output)
+  const float* cosv;
+  const float* sinv;  // [HD/2] at pos
+  __half* kc;
+  __half* vc;  // [B, H, ctx, HD]
+  float* part;  // [B*H][nsplit][HD + 2] partial (acc, m, l)
+  int* cnt;     // [B*H] arrival counters (left at 0)
+  float* out;   // [B, H * HD]
+  int B, H, ctx, pos, nsplit;
+  float scale;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
+  __shared__ __align__(128) __half ks[kAttnChunk * HD];
+  __shared__ __align__(128) __half vs[kAttnChunk * HD];
+  __shared__ float qs[HD];
+  __shared__ float ps[kAttnChunk];
+  __shared__ float red[2];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int last;
+  const int split = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / a.H, h = bh % a.H;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int p0 = split * kAttnChunk;
+  const int p1 = min(p0 + kAttnChunk, a.pos + 1);  // positions [p0, p1)
+  const int pe = min(p1, a.pos);                    // cached rows [p0, pe)
+  asm volatile("griddepcontrol.launch_dependents;");
+  const size_t row0 = ((size_t)bh * a.ctx + p0) * HD;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (pe > p0) {
+      const uint32_t bytes = (uint32_t)((pe - p0) * HD * 2);
+      mbar_expect_tx(&bar, 2 * bytes);
+      bulk_g2s(ks, a.kc + row0, bytes, &bar);
+      bulk_g2s(vs, a.vc + row0, bytes, &bar);
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // q, k, v of the new token
+  const float* q = a.qkv + ((size_t)(b * 3 + 0) * a.H + h) * HD;
+  const float* k = a.qkv + ((size_t)(b * 3 + 1) * a.H + h) * HD;
+  const float* v = a.qkv + ((size_t)(b * 3 + 2) * a.H + h) * HD;
+  constexpr int half = HD / 2;
+  const bool mine = a.pos >= p0 && a.pos < p0 + kAttnChunk;  // this chunk holds the new token
+  for (int i = tid; i < half; i += blockDim.x) {
+    const float c = a.cosv[i], s = a.sinv[i];
+    // q rounded through f16 like the cache (the attention inputs are f16)
+    qs[i] = __half2float(__float2half_rn(q[i] * c - q[i + half] * s));
+    qs[i + half] = __half2float(__float2half_rn(q[i + half] * c + q[i] * s));
+    if (mine) {
+      const __half k0 = __float2half_rn(k[i] * c - k[i + half] * s);
+      const __half k1 = __float2half_rn(k[i + half] * c + k[i] * s);
+      const __half v0 = __float2half_rn(v[i]), v1 = __float2half_rn(v[i + half]);
+      const int r = (a.pos - p0) * HD;
+      ks[r + i] = k0;
+      ks[r + i + half] = k1;
+      vs[r + i] = v0;
+      vs[r + i + half] = v1;
+      const size_t g = ((size_t)bh * a.ctx + a.pos) * HD;
+      a.kc[g + i] = k0;
+      a.kc[g + i + half] = k1;
+      a.vc[g + i] = v0;
+      a.vc[g + i + half] = v1;
+    }
+  }
+  if (pe > p0) mbar_wait(&bar, 0);
+  __syncthreads();
+  // scores: a warp per position, lanes over the head dimension
+  const int n = p1 - p0;
+  constexpr int DPL = HD / 32;  // dims per lane
+  for (int j = warp; j < n; j += blockDim.x / 32) {
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc += qs[lane * DPL + e] * __half2float(ks[j * HD + lane * DPL + e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ps[j] = acc * a.scale;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float m = -INFINITY;
+    for (int j = lane; j < n; j += 32) m = fmaxf(m, ps[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float e = __expf(ps[j] - m);
+      ps[j] = e;
+      l += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) {
+      red[0] = m;
+      red[1] = l;
+    }
+  }
+  __syncthreads();
+  float* pp = a.part + ((size_t)bh * a.nsplit + split) * (HD + 2);
+  for (int d = tid; d < HD; d += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < n; ++j) acc += ps[j] * __half2float(vs[j * HD + d]);
+    pp[d] = acc;
+  }
+  if (tid == 0) {
+    pp[HD] = red[0];
+    pp[HD + 1] = red[1];
+  }
+  // the last CTA of this (sequence, head) combines the partials in split order
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(&a.cnt[bh], 1) == a.nsplit - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* P = a.part + (size_t)bh * a.nsplit * (HD + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, P[s * (HD + 2) + HD]);
+  float L = 0.f;
+  for (int s = 0; s < a.nsplit; ++s) L += __expf(P[s * (HD + 2) + HD] - M) * P[s * (HD + 2) + HD + 1];
+  const float inv = 1.f / L;
+  for (int d = tid; d < HD; d += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < a.nsplit; ++s) acc += __expf(P[s * (HD + 2) + HD] - M) * P[s * (HD + 2) + d];
+    a.out[(size_t)b * a.H * HD + h * HD + d] = acc * inv;
+  }
+  if (tid == 0) a.cnt[bh] = 0;
+}
+
 }  // namespace qigen
 
 using namespace qigen;
+
+extern "C" int64_t qigen_attn_decode_workspace_size(int64_t batch, int64_t heads, int64_t head_dim,
+                                                    int64_t ctx) {
+  const int64_t nsplit = (ctx + kAttnChunk - 1) / kAttnChunk;
+  return batch * heads * (nsplit * (head_dim + 2) * 4 + 4) + 256;
+}
+
+extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
+                                 const float* cos_pos, const float* sin_pos, void* k_cache,
+                                 void* v_cache, int64_t ctx, int64_t pos, float scale, float* out,
+                                 void* workspace, int64_t workspace_bytes, void* stream) {
+  QIGEN_CHECK_ARG(qkv && cos_pos && sin_pos && k_cache && v_cache && out && workspace,
+                  QIGEN_ERR_ARG, "null pointer");
+  QIGEN_CHECK_ARG(head_dim == 64 || head_dim == 128, QIGEN_ERR_UNSUPPORTED,
+                  "decode attention takes head_dim 64 or 128, got %lld", (long long)head_dim);
+  QIGEN_CHECK_ARG(pos >= 0 && pos < ctx && batch > 0 && heads > 0, QIGEN_ERR_ARG,
+                  "bad position / shape");
+  QIGEN_CHECK_ARG(workspace_bytes >= qigen_attn_decode_workspace_size(batch, heads, head_dim, ctx),
+                  QIGEN_ERR_ARG, "attention workspace too small");
+  AttnArgs a;
+  a.qkv = qkv;
+  a.cosv = cos_pos;
+  a.sinv = sin_pos;
+  a.kc = (__half*)k_cache;
+  a.vc = (__half*)v_cache;
+  a.B = (int)batch;
+  a.H = (int)heads;
+  a.ctx = (int)ctx;
+  a.pos = (int)pos;
+  a.nsplit = (int)((pos + 1 + kAttnChunk - 1) / kAttnChunk);
+  a.scale = scale;
+  a.out = out;
+  // counters first (zero-initialised by the caller, left at zero by the kernel)
+  a.cnt = (int*)workspace;
+  a.part = (float*)((char*)workspace + ((batch * heads * 4 + 255) / 256) * 256);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.nsplit, (unsigned)(batch * heads), 1);
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute pa;
+  pa.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pa.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &pa;
+  cfg.numAttrs = 1;
+  if (head_dim == 128) QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<128>, a));
+  else QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<64>, a));
+  return QIGEN_OK;
+}
 
 extern "C" int qigen_rope_kv(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
                              const float* cos_pos, const float* sin_pos, void* q_out,

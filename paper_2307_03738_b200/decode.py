@@ -163,6 +163,20 @@ class GpuBackend:
              _dev.stream_handle())
 
     @staticmethod
+    def attention(qkv, cos, sin, k_cache, v_cache, pos, scale, out, workspace):
+        """RoPE + KV append + split-KV attention in one kernel (decode_ops.cu)."""
+        B, H, ctx, hd = k_cache.shape
+        call("qigen_attn_decode", qkv.data_ptr(), B, H, hd, cos.data_ptr(), sin.data_ptr(),
+             k_cache.data_ptr(), v_cache.data_ptr(), ctx, pos, float(scale), out.data_ptr(),
+             workspace.data_ptr(), workspace.numel(), _dev.stream_handle())
+
+    @staticmethod
+    def attention_workspace(B, H, hd, ctx, device):
+        from ._lib import lib
+        n = int(lib().qigen_attn_decode_workspace_size(B, H, hd, ctx))
+        return torch.zeros(n, dtype=torch.uint8, device=device)
+
+    @staticmethod
     def rmsnorm_f16(h, w, eps, out):
         call("qigen_rmsnorm_f16", h.data_ptr(), w.data_ptr(), h.shape[0], h.shape[1], float(eps),
              out.data_ptr(), _dev.stream_handle())
@@ -241,6 +255,7 @@ class LlamaTP:
                 g = randn((batch, cfg.n_heads, max_ctx, hd), 10_000_000 + 2 * li + j) * 50.0
                 cache[li] = g[:, self.h0:self.h1].to(kv_dtype)
                 del g
+        self.attn_ws = backend.attention_workspace(batch, self.nh, hd, max_ctx, self.dev)
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device=self.dev).float() / hd))
         ang = torch.arange(max_ctx, device=self.dev).float()[:, None] * inv[None, :]
         self.cos, self.sin = ang.cos(), ang.sin()  # [ctx, hd/2]
@@ -260,21 +275,20 @@ class LlamaTP:
     def step(self, tokens: torch.Tensor, pos: int) -> torch.Tensor:
         """Greedy next tokens for `tokens` [B] at position `pos` (static shapes:
         graph-capturable for a fixed pos).  Per layer: QKV GEMV (RMSNorm fused
-        into its prologue) -> RoPE + KV append -> attention -> o_proj GEMV
+        into its prologue) -> fused RoPE + KV append + attention -> o_proj GEMV
         (residual fused, all-reduce) -> gate|up GEMV (RMSNorm fused) -> down
         GEMV (SwiGLU fused, residual fused, all-reduce)."""
         cfg, B, hd, be = self.cfg, self.B, self.cfg.head_dim, self.backend
         h = self.embed[tokens].float()                     # [B, d] residual stream
         cos, sin = self.cos[pos], self.sin[pos]
-        q16 = torch.empty((B, self.nh, 1, hd), dtype=self.k_cache.dtype, device=self.dev)
         scale = 1.0 / math.sqrt(hd)
+        att = torch.empty((B, self.nh * hd), dtype=torch.float32, device=self.dev)
         for li, lay in enumerate(self.layers):
             qkv = lay["qkv"](h, prologue="rmsnorm", norm_weight=lay["n1"], eps=cfg.norm_eps)
-            be.rope_kv(qkv, cos, sin, q16, self.k_cache[li], self.v_cache[li], pos)
-            kc = self.k_cache[li, :, :, : pos + 1]
-            vc = self.v_cache[li, :, :, : pos + 1]
-            att = F.scaled_dot_product_attention(q16, kc, vc, scale=scale)  # [B, H_l, 1, hd]
-            h = self._row_parallel(lay["o"], att.reshape(B, self.nh * hd), h)
+            # RoPE + KV append + attention over positions 0..pos
+            be.attention(qkv, cos, sin, self.k_cache[li], self.v_cache[li], pos, scale, att,
+                         self.attn_ws)
+            h = self._row_parallel(lay["o"], att, h)
             gu = lay["gu"](h, prologue="rmsnorm", norm_weight=lay["n2"], eps=cfg.norm_eps)
             h = self._row_parallel(lay["down"], gu, h, prologue="swiglu")
         xn = torch.empty((B, cfg.d_model), dtype=torch.float16, device=self.dev)

@@ -55,6 +55,21 @@ class OracleBackend:
         k_cache[:, :, pos] = rot(k).to(k_cache.dtype)
         v_cache[:, :, pos] = v.to(v_cache.dtype)
 
+    @classmethod
+    def attention(cls, qkv, cos, sin, k_cache, v_cache, pos, scale, out, workspace):
+        """RoPE + KV append, then torch SDPA over the f16 (or f32) cache."""
+        B, H, ctx, hd = k_cache.shape
+        q = torch.empty((B, H, 1, hd), dtype=k_cache.dtype, device=k_cache.device)
+        cls.rope_kv(qkv, cos, sin, q, k_cache, v_cache, pos)
+        att = torch.nn.functional.scaled_dot_product_attention(
+            q.float(), k_cache[:, :, : pos + 1].float(), v_cache[:, :, : pos + 1].float(),
+            scale=scale)
+        out.copy_(att.reshape(B, H * hd))
+
+    @staticmethod
+    def attention_workspace(B, H, hd, ctx, device):
+        return None
+
     @staticmethod
     def rmsnorm_f16(h, w, eps, out):
         out.copy_(h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + eps) * w)
