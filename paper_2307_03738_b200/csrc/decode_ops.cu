@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
       bulk_g2s(vs, a.vc + row0, bytes, &bar);
     }
   }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
   asm volatile("griddepcontrol.wait;" ::: "memory");  // q, k, v of the new token
   const float* q = a.qkv + ((size_t)(b * 3 + 0) * a.H + h) * HD;
   const float* k = a.qkv + ((size_t)(b * 3 + 1) * a.H + h) * HD;
@@ -130,12 +131,16 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   const bool mine = a.pos >= p0 && a.pos < p0 + kAttnChunk;  // this chunk holds the new token
   for (int i = tid; i < half; i += blockDim.x) {
     const float c = a.cosv[i], s = a.sinv[i];
-    // q rounded through f16 like the cache (the attention inputs are f16)
-    qs[i] = __half2float(__float2half_rn(q[i] * c - q[i + half] * s));
-    qs[i + half] = __half2float(__float2half_rn(q[i + half] * c + q[i] * s));
+    // rotate-half with separately rounded products (no FMA contraction: the
+    // same f32 results as an elementwise implementation); q rounded through
+    // f16 like the cache (the attention inputs are f16)
+    auto rot_lo = [&](float x0, float x1) { return __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s)); };
+    auto rot_hi = [&](float x0, float x1) { return __fadd_rn(__fmul_rn(x1, c), __fmul_rn(x0, s)); };
+    qs[i] = __half2float(__float2half_rn(rot_lo(q[i], q[i + half])));
+    qs[i + half] = __half2float(__float2half_rn(rot_hi(q[i], q[i + half])));
     if (mine) {
-      const __half k0 = __float2half_rn(k[i] * c - k[i + half] * s);
-      const __half k1 = __float2half_rn(k[i + half] * c + k[i] * s);
+      const __half k0 = __float2half_rn(rot_lo(k[i], k[i + half]));
+      const __half k1 = __float2half_rn(rot_hi(k[i], k[i + half]));
       const __half v0 = __float2half_rn(v[i]), v1 = __float2half_rn(v[i + half]);
       const int r = (a.pos - p0) * HD;
       ks[r + i] = k0;

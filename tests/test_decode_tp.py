@@ -106,3 +106,29 @@ def test_gpu_decode_matches_oracle_backend():
         # the caches got the same new entries
         assert torch.allclose(ref.k_cache[:, :, :, 40].float(), gpu.k_cache[:, :, :, 40].float(),
                               atol=2e-3, rtol=2e-3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,H,ctx,pos", [(1, 32, 513, 512), (1, 64, 1025, 1024), (2, 8, 100, 70),
+                                         (1, 64, 1025, 500), (3, 4, 64, 0), (1, 8, 200, 63)])
+def test_fused_attention_vs_sdpa(B, H, ctx, pos):
+    """qigen_attn_decode (RoPE + KV append + split-KV attention) against RoPE
+    + torch SDPA; the appended cache rows are bit-identical."""
+    import math
+    from decode_backends import OracleBackend
+    hd = 128
+    g = torch.Generator(device="cuda").manual_seed(B * 1000 + H + pos)
+    qkv = torch.randn(B, 3 * H * hd, device="cuda", generator=g)
+    ang = torch.rand(hd // 2, device="cuda", generator=g) * 6
+    cos, sin = ang.cos(), ang.sin()
+    kc = torch.randn(B, H, ctx, hd, device="cuda", generator=g).half()
+    vc = torch.randn(B, H, ctx, hd, device="cuda", generator=g).half()
+    kc2, vc2 = kc.clone(), vc.clone()
+    out = torch.empty(B, H * hd, device="cuda")
+    ref = torch.empty(B, H * hd, device="cuda")
+    ws = D.GpuBackend.attention_workspace(B, H, hd, ctx, "cuda")
+    for _ in range(2):  # the workspace is reusable
+        D.GpuBackend.attention(qkv, cos, sin, kc, vc, pos, 1 / math.sqrt(hd), out, ws)
+    OracleBackend.attention(qkv, cos, sin, kc2, vc2, pos, 1 / math.sqrt(hd), ref, None)
+    assert ((out - ref).abs().max() / (1 + ref.abs().max())).item() < 1e-5
+    assert torch.equal(kc, kc2) and torch.equal(vc, vc2)
