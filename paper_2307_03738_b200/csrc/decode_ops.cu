@@ -93,7 +93,16 @@ struct AttnArgs {
   float* out;   // [B, H * HD]
   int B, H, ctx, pos, nsplit;
   float scale;
+  unsigned long long* trace;  // optional per-CTA %globaltimer: entry, after wait, exit
 };
+
+__device__ __forceinline__ void attn_trace(const AttnArgs& a, int i) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 4 + i] = t;
+  }
+}
 
 template <int HD>
 __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
@@ -110,6 +119,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   const int p0 = split * kAttnChunk;
   const int p1 = min(p0 + kAttnChunk, a.pos + 1);  // positions [p0, p1)
   const int pe = min(p1, a.pos);                    // cached rows [p0, pe)
+  attn_trace(a, 0);
   asm volatile("griddepcontrol.launch_dependents;");
   const size_t row0 = ((size_t)bh * a.ctx + p0) * HD;
   if (tid == 0) {
@@ -124,6 +134,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   }
   __syncthreads();  // the barrier is initialised before anyone waits on it
   asm volatile("griddepcontrol.wait;" ::: "memory");  // q, k, v of the new token
+  attn_trace(a, 1);
   const float* q = a.qkv + ((size_t)(b * 3 + 0) * a.H + h) * HD;
   const float* k = a.qkv + ((size_t)(b * 3 + 1) * a.H + h) * HD;
   const float* v = a.qkv + ((size_t)(b * 3 + 2) * a.H + h) * HD;
@@ -202,25 +213,54 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   __syncthreads();
   if (tid == 0) last = atomicAdd(&a.cnt[bh], 1) == a.nsplit - 1;
   __syncthreads();
+  attn_trace(a, 2);
   if (!last) return;
   __threadfence();
+  // all partials in one round trip: (m, l) of every split into shared memory,
+  // then each thread its dimension of every split (independent loads)
   const float* P = a.part + (size_t)bh * a.nsplit * (HD + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, P[s * (HD + 2) + HD]);
-  float L = 0.f;
-  for (int s = 0; s < a.nsplit; ++s) L += __expf(P[s * (HD + 2) + HD] - M) * P[s * (HD + 2) + HD + 1];
-  const float inv = 1.f / L;
+  float* msh = ps;  // reuse: [nsplit] weights exp(m_s - M) (nsplit <= kAttnChunk here)
+  __shared__ float lsh[kAttnChunk];
+  for (int s = tid; s < a.nsplit; s += blockDim.x) {
+    msh[s] = __ldcg(P + s * (HD + 2) + HD);
+    lsh[s] = __ldcg(P + s * (HD + 2) + HD + 1);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float M = -INFINITY;
+    for (int s = lane; s < a.nsplit; s += 32) M = fmaxf(M, msh[s]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    for (int s = lane; s < a.nsplit; s += 32) {
+      const float e = __expf(msh[s] - M);
+      msh[s] = e;
+      L += e * lsh[s];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) red[1] = 1.f / L;
+  }
+  __syncthreads();
+  const float inv = red[1];
   for (int d = tid; d < HD; d += blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < a.nsplit; ++s) acc += __expf(P[s * (HD + 2) + HD] - M) * P[s * (HD + 2) + d];
+    for (int s = 0; s < a.nsplit; ++s) acc += msh[s] * __ldcg(P + s * (HD + 2) + d);
     a.out[(size_t)b * a.H * HD + h * HD + d] = acc * inv;
   }
   if (tid == 0) a.cnt[bh] = 0;
+  attn_trace(a, 3);
 }
 
 }  // namespace qigen
 
 using namespace qigen;
+
+static unsigned long long* g_attn_trace = nullptr;
+extern "C" int qigen_debug_attn_trace(void* buf) {
+  g_attn_trace = (unsigned long long*)buf;
+  return QIGEN_OK;
+}
 
 extern "C" int64_t qigen_attn_decode_workspace_size(int64_t batch, int64_t heads, int64_t head_dim,
                                                     int64_t ctx) {
@@ -238,6 +278,8 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
                   "decode attention takes head_dim 64 or 128, got %lld", (long long)head_dim);
   QIGEN_CHECK_ARG(pos >= 0 && pos < ctx && batch > 0 && heads > 0, QIGEN_ERR_ARG,
                   "bad position / shape");
+  QIGEN_CHECK_ARG((pos + kAttnChunk) / kAttnChunk <= kAttnChunk, QIGEN_ERR_UNSUPPORTED,
+                  "decode attention supports up to %d positions", kAttnChunk * kAttnChunk);
   QIGEN_CHECK_ARG(workspace_bytes >= qigen_attn_decode_workspace_size(batch, heads, head_dim, ctx),
                   QIGEN_ERR_ARG, "attention workspace too small");
   AttnArgs a;
@@ -253,6 +295,7 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
   a.nsplit = (int)((pos + 1 + kAttnChunk - 1) / kAttnChunk);
   a.scale = scale;
   a.out = out;
+  a.trace = g_attn_trace;
   // counters first (zero-initialised by the caller, left at zero by the kernel)
   a.cnt = (int*)workspace;
   a.part = (float*)((char*)workspace + ((batch * heads * 4 + 255) / 256) * 256);
@@ -265,6 +308,14 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
   pa.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &pa;
   cfg.numAttrs = 1;
+  static bool configured = false;
+  if (!configured) {  // same shared-memory carveout as the GEMVs around it
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(attn_decode_kernel<128>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(attn_decode_kernel<64>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    configured = true;
+  }
   if (head_dim == 128) QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<128>, a));
   else QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<64>, a));
   return QIGEN_OK;

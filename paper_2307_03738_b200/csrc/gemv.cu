@@ -52,6 +52,10 @@ struct GemvArgs {
   int x_vec;         // x rows 16-byte aligned -> vector loads
   int accumulate;
   int x_ready;       // x is not written by the preceding kernel: read it before the PDL wait
+  int l2_self;       // L2-prefetch this CTA's weights beyond the first ring fill at entry
+  const char* pf_ptr[2];  // L2 prefetch hint for the NEXT kernel's data (split over CTAs)
+  int64_t pf_bytes[2];
+  int pf_when;            // 0: at entry, 1: after the main loop
   int max_steps;     // max K-steps (32 rows) of any chunk
   int D;             // ring stages per warp
   int pre;           // stages per warp issued before griddepcontrol.wait
@@ -135,10 +139,19 @@ __device__ __forceinline__ void row_inv_rms(const GemvArgs& a, int t0, int ntok,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = 0; j < ntok; ++j) {
     float ss = 0.f;
-    for (int64_t k = 4 * threadIdx.x; k < a.n; k += 4 * T) {
-      float v[4];
-      load_raw4(a, (t0 + j) * a.ldx + k, k, v);
-      ss += v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
+    // batches of 8 independent loads per thread: one L2 round trip per batch
+    // (a 4096-wide row at T = 256 is a single batch)
+    for (int64_t kb = 4 * threadIdx.x; kb < a.n; kb += 32 * T) {
+      float v[8][4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t k = kb + (int64_t)u * 4 * T;
+        if (k < a.n) load_raw4(a, (t0 + j) * a.ldx + k, k, v[u]);
+        else v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        ss += v[u][0] * v[u][0] + v[u][1] * v[u][1] + v[u][2] * v[u][2] + v[u][3] * v[u][3];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -264,7 +277,27 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     for (int i = 0; i < D; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < n_pre; ++s) issue(s);
+    if (a.l2_self && nks > n_first) {
+      // the rest of this warp's chunk streams into L2 now, so the ring refills
+      // after the PDL wait hit L2 instead of waiting on DRAM
+      bulk_prefetch_l2(wsrc + (int64_t)(ks0 + n_first) * BITS * 512,
+                       (uint32_t)((nks - n_first) * BITS * 512));
+      if (SZB) bulk_prefetch_l2(zsrc + (int64_t)(ks0 + n_first) * SZB, (uint32_t)((nks - n_first) * SZB));
+    }
   }
+  auto prefetch_next = [&]() {  // this CTA's slice of the next kernel's data
+    if (threadIdx.x != 0) return;
+    const int64_t nctas = (int64_t)gridDim.x * gridDim.y;
+    const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    for (int r = 0; r < 2; ++r) {
+      if (!a.pf_ptr[r] || a.pf_bytes[r] <= 0) continue;
+      const int64_t per = ((a.pf_bytes[r] + nctas - 1) / nctas + 15) / 16 * 16;
+      const int64_t b0 = cta * per, b1 = min(a.pf_bytes[r], b0 + per);
+      for (int64_t o = b0; o < b1; o += 65536)
+        bulk_prefetch_l2(a.pf_ptr[r] + o, (uint32_t)min((int64_t)65536, b1 - o));
+    }
+  };
+  if (a.pf_when == 0) prefetch_next();
   if (threadIdx.x < 2) ((uint32_t*)(smem + L.zero))[threadIdx.x] = 0u;
   uint64_t* rbar = (uint64_t*)(smem + L.rbar);
   uint64_t* pbar = (uint64_t*)(smem + L.pbar);
@@ -328,23 +361,38 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     uint32_t* bw = (uint32_t*)(smem + L.bfrag);
     const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
     bool first = true;
-    for (int it0 = 0; it0 < items; it0 += T) {  // CTA-uniform trip count
-      const int it = it0 + threadIdx.x;
-      const bool live = it < items;
-      const int sub = it & 7, st = (it >> 3) % nsteps, tk = live ? (it >> 3) / nsteps : 0;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (live) load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v, inv_rms);
+    // rounds of T items (at most 2 here, more go to act_prep_kernel): all the
+    // loads of a batch of rounds are issued before any is digitised, so the
+    // prologue pays one L2 round trip, not one per round
+    for (int r0 = 0; r0 * T < items; r0 += 2) {  // CTA-uniform trip count
+      float v[2][4];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int it = (r0 + r) * T + threadIdx.x;
+        v[r][0] = v[r][1] = v[r][2] = v[r][3] = 0.f;
+        if (it < items) {
+          const int sub = it & 7, st = (it >> 3) % nsteps, tk = (it >> 3) / nsteps;
+          load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v[r], inv_rms);
+        }
+      }
       if (first) {  // the rest of the first ring fill goes out behind the x loads
         trace_point(a, 8);
         first = false;
         if (lane == 0)
           for (int s = n_pre; s < n_first; ++s) issue(s);
       }
-      const Digits d = digitize<IPU>(v, umask);
-      if (it0 == 0) trace_point(a, 11);
-      if (live) {
-        store_digits(bw, st, tk, TP, sub, d);
-        if ((it % IPU) == 0) xs[((it % (nsteps * 8)) / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if ((r0 + r) * T >= items) break;  // CTA-uniform
+        const int it = (r0 + r) * T + threadIdx.x;
+        const bool live = it < items;
+        const int sub = it & 7, st = (it >> 3) % nsteps, tk = live ? (it >> 3) / nsteps : 0;
+        const Digits d = digitize<IPU>(v[r], umask);
+        if (r0 + r == 0) trace_point(a, 11);
+        if (live) {
+          store_digits(bw, st, tk, TP, sub, d);
+          if ((it % IPU) == 0) xs[((it % (nsteps * 8)) / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
+        }
       }
     }
     // zero fragments / unit params of the padding tokens M..TP-1
@@ -463,6 +511,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     }
   }
   trace_point(a, 3);
+  if (a.pf_when == 1) prefetch_next();
 
   // ---- 5. combine digit-pair lanes; deterministic split-K reduction ---------
   // Element e = (warp*16 + row)*M + token of this CTA column.  With S > 1 the
@@ -515,6 +564,11 @@ static int g_policy = 0;      // tuning: L2 evict_first hint on weight copies
 static int g_wpc = 8;         // tuning: warps per CTA for <= 4 tokens (8 or 16)
 static int g_ring_kb = 0;     // tuning: ring bytes per CTA (KB; 0 = 10 KB per warp)
 static int g_max_ctas = 0;    // tuning: cap on the grid (0 = rule below)
+static int g_l2_self = 0;     // tuning: L2-prefetch each CTA's weights beyond the ring at entry
+static int g_pf_when = 1;
+static int g_max_split = kMaxSplits;  // tuning: cap on the cluster (K split) size     // tuning: when the next-kernel L2 hint is issued (0 entry, 1 after loop)
+static thread_local const void* t_pf_ptr[2] = {nullptr, nullptr};
+static thread_local int64_t t_pf_bytes[2] = {0, 0};
 
 static int sm_count() {
   static int cached = 0;
@@ -561,6 +615,9 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    // every kernel of a decode chain asks for the same (maximal) shared-memory
+    // carveout, so consecutive kernels can share an SM without a reconfiguration
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     configured = true;
   }
   const int stage = BITS * 512 + GPS * 128;
@@ -620,9 +677,11 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     for (int c = 2; c <= std::min(kMaxSplits, a.KS); ++c)
       if (cols * c <= g_max_ctas && (a.KS + c - 1) / c >= 2) S = c;
   }
+  if (req_S <= 0) S = std::min(S, g_max_split);
   QIGEN_CHECK_ARG(S >= 1 && S <= a.KS && S <= kMaxSplits, QIGEN_ERR_ARG, "k_splits %d out of range", S);
   // many tokens x long chunks: split K further until the fragments fit in smem
   while (req_S <= 0 && shape(S).total > 200 * 1024 && S < std::min(kMaxSplits, a.KS)) ++S;
+  // (the smem-fit rule above may exceed g_max_split: fitting wins)
   const SmemLayout L = shape(S);
   a.pre = g_pre < 0 ? a.D : g_pre;
   QIGEN_CHECK_ARG(L.total <= 227 * 1024, QIGEN_ERR_UNSUPPORTED,
@@ -649,6 +708,12 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     pa.val.programmaticStreamSerializationAllowed = 1;
     pc.attrs = &pa;
     pc.numAttrs = 1;
+    static bool prep_configured = false;
+    if (!prep_configured) {
+      QIGEN_CUDA_RET(cudaFuncSetAttribute(act_prep_kernel<IPU>,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      prep_configured = true;
+    }
     QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_kernel<IPU>, a, (int)TP, (int)UPS));
   }
   cudaLaunchConfig_t cfg = {};
@@ -709,6 +774,29 @@ extern "C" int qigen_debug_trace(void* buf) {
 
 extern "C" int qigen_debug_prefetch(int stages_before_wait) {
   g_pre = stages_before_wait;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_gemv_prefetch_next(const void* p0, int64_t bytes0, const void* p1,
+                                        int64_t bytes1) {
+  QIGEN_CHECK_ARG(bytes0 >= 0 && bytes1 >= 0 && (bytes0 % 16) == 0 && (bytes1 % 16) == 0 &&
+                      ((uintptr_t)p0 % 16) == 0 && ((uintptr_t)p1 % 16) == 0,
+                  QIGEN_ERR_ARG, "prefetch ranges must be 16-byte aligned and sized");
+  t_pf_ptr[0] = p0;
+  t_pf_bytes[0] = p0 ? bytes0 : 0;
+  t_pf_ptr[1] = p1;
+  t_pf_bytes[1] = p1 ? bytes1 : 0;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_max_split(int s) {
+  g_max_split = s < 1 ? 1 : (s > kMaxSplits ? kMaxSplits : s);
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_l2_prefetch(int self, int when) {
+  g_l2_self = self;
+  g_pf_when = when;
   return QIGEN_OK;
 }
 
@@ -789,6 +877,14 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   a.x_ready = (accumulate & QIGEN_GEMV_X_READY) ? 1 : 0;
   a.trace = g_trace;
   a.trace_clk = g_trace_clk;
+  a.l2_self = g_l2_self;
+  a.pf_when = g_pf_when;
+  for (int r = 0; r < 2; ++r) {  // consume the one-shot hint of qigen_gemv_prefetch_next
+    a.pf_ptr[r] = (const char*)t_pf_ptr[r];
+    a.pf_bytes[r] = t_pf_bytes[r];
+    t_pf_ptr[r] = nullptr;
+    t_pf_bytes[r] = 0;
+  }
   a.early = g_early || a.x_ready;  // independent x: overlap the predecessor fully
   a.policy = g_policy;
   const int S = k_splits;  // 0: chosen per launch shape in launch_cfg

@@ -20,13 +20,15 @@ qkvs = [torch.empty(1, 3 * cfg.d_model, device="cuda") for _ in range(L)]
 gus = [torch.empty(1, 2 * cfg.ffn, device="cuda") for _ in range(L)]
 
 
-def full():
+def full(pf=False):
     for li, lay in enumerate(m.layers):
-        lay["qkv"](h, out=qkvs[li], prologue="rmsnorm", norm_weight=lay["n1"])
+        nx = m.layers[(li + 1) % L]["qkv"]
+        k = (lambda t: {"prefetch": t}) if pf else (lambda t: {})
+        lay["qkv"](h, out=qkvs[li], prologue="rmsnorm", norm_weight=lay["n1"], **k(lay["o"]))
         be.attention(qkvs[li], cos, sin, m.k_cache[li], m.v_cache[li], pos, 1 / math.sqrt(128), att, m.attn_ws)
-        lay["o"](att, out=h, accumulate=True)
-        lay["gu"](h, out=gus[li], prologue="rmsnorm", norm_weight=lay["n2"])
-        lay["down"](gus[li], out=h, accumulate=True, prologue="swiglu")
+        lay["o"](att, out=h, accumulate=True, **k(lay["gu"]))
+        lay["gu"](h, out=gus[li], prologue="rmsnorm", norm_weight=lay["n2"], **k(lay["down"]))
+        lay["down"](gus[li], out=h, accumulate=True, prologue="swiglu", **k(nx))
 
 
 def gemvs():
@@ -51,13 +53,28 @@ def attn():
         be.attention(qkvs[li], cos, sin, m.k_cache[li], m.v_cache[li], pos, 1 / math.sqrt(128), att, m.attn_ws)
 
 
+import os
+Lb = _lib.lib()
 s = torch.cuda.Stream()
-for name, fn in [("full layer", full), ("4 gemvs", gemvs),
+def base():
+    Lb.qigen_debug_l2_prefetch(0, 1); full(pf=False)
+variants = [("full layer", base)]
+for ms in [1, 2, 3, 4, 8]:
+    def f(ms=ms):
+        Lb.qigen_debug_max_split(ms)
+        full(pf=False)
+        Lb.qigen_debug_max_split(16)
+    variants.append((f"max split {ms}", f))
+def reset():
+    Lb.qigen_debug_l2_prefetch(0, 1)
+if os.environ.get("ALL"):
+  variants += [("4 gemvs", gemvs),
                  ("qkv (rmsnorm)", one("qkv", prologue="rmsnorm", norm_weight=m.layers[0]["n1"])),
                  ("o (acc)", one("o", accumulate=True)),
                  ("gate_up (rmsnorm)", one("gu", prologue="rmsnorm", norm_weight=m.layers[0]["n2"])),
                  ("down (swiglu, acc)", one("down", prologue="swiglu", accumulate=True)),
-                 ("attention", attn)]:
+                 ("attention", attn)]
+for name, fn in variants:
     with torch.cuda.stream(s):
         fn(); s.synchronize()
         g = torch.cuda.CUDAGraph()
