@@ -223,6 +223,8 @@ int qigen_debug_force_prep(int on);
 int qigen_debug_l2_prefetch(int self, int when);
 /* Tuning aid: cap the automatic K split (thread-block cluster size) of the GEMV. */
 int qigen_debug_max_split(int s);
+/* Tuning aid: preferred shared-memory carveout (percent, -1 = driver default) of the GEMV. */
+int qigen_debug_carveout(int pct);
 /* Tuning aid: L2 evict_first on weight copies, warps per CTA (8/16), ring KB per CTA, grid cap. */
 int qigen_debug_gemv_tuning(int policy, int wpc, int ring_kb, int max_ctas);
 int qigen_debug_early_trigger(int on);

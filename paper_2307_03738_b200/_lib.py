@@ -61,6 +61,7 @@ SIGNATURES = {
     "qigen_gemv_prefetch_next": (_I32, [_P, _I64, _P, _I64]),
     "qigen_debug_l2_prefetch": (_I32, [_I32, _I32]),
     "qigen_debug_max_split": (_I32, [_I32]),
+    "qigen_debug_carveout": (_I32, [_I32]),
     "qigen_gemv_group_create": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
     "qigen_gemv_group_run": (_I32, [_P, _P]),
     "qigen_gemv_group_destroy": (_I32, [_P]),

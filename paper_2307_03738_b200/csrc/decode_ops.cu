@@ -308,14 +308,6 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
   pa.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &pa;
   cfg.numAttrs = 1;
-  static bool configured = false;
-  if (!configured) {  // same shared-memory carveout as the GEMVs around it
-    QIGEN_CUDA_RET(cudaFuncSetAttribute(attn_decode_kernel<128>,
-                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    QIGEN_CUDA_RET(cudaFuncSetAttribute(attn_decode_kernel<64>,
-                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    configured = true;
-  }
   if (head_dim == 128) QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<128>, a));
   else QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<64>, a));
   return QIGEN_OK;

@@ -564,7 +564,6 @@ static int launch(TcArgs& a, int req_S, void* ws, cudaStream_t stream, const voi
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     configured = true;
   }
   const int cols = (a.P + kPanels - 1) / kPanels;

@@ -139,19 +139,10 @@ __device__ __forceinline__ void row_inv_rms(const GemvArgs& a, int t0, int ntok,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = 0; j < ntok; ++j) {
     float ss = 0.f;
-    // batches of 8 independent loads per thread: one L2 round trip per batch
-    // (a 4096-wide row at T = 256 is a single batch)
-    for (int64_t kb = 4 * threadIdx.x; kb < a.n; kb += 32 * T) {
-      float v[8][4];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t k = kb + (int64_t)u * 4 * T;
-        if (k < a.n) load_raw4(a, (t0 + j) * a.ldx + k, k, v[u]);
-        else v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        ss += v[u][0] * v[u][0] + v[u][1] * v[u][1] + v[u][2] * v[u][2] + v[u][3] * v[u][3];
+    for (int64_t k = 4 * threadIdx.x; k < a.n; k += 4 * T) {
+      float v[4];
+      load_raw4(a, (t0 + j) * a.ldx + k, k, v);
+      ss += v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -361,38 +352,23 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     uint32_t* bw = (uint32_t*)(smem + L.bfrag);
     const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
     bool first = true;
-    // rounds of T items (at most 2 here, more go to act_prep_kernel): all the
-    // loads of a batch of rounds are issued before any is digitised, so the
-    // prologue pays one L2 round trip, not one per round
-    for (int r0 = 0; r0 * T < items; r0 += 2) {  // CTA-uniform trip count
-      float v[2][4];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int it = (r0 + r) * T + threadIdx.x;
-        v[r][0] = v[r][1] = v[r][2] = v[r][3] = 0.f;
-        if (it < items) {
-          const int sub = it & 7, st = (it >> 3) % nsteps, tk = (it >> 3) / nsteps;
-          load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v[r], inv_rms);
-        }
-      }
+    for (int it0 = 0; it0 < items; it0 += T) {  // CTA-uniform trip count
+      const int it = it0 + threadIdx.x;
+      const bool live = it < items;
+      const int sub = it & 7, st = (it >> 3) % nsteps, tk = live ? (it >> 3) / nsteps : 0;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (live) load_x4(a, tk, k0 + 32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v, inv_rms);
       if (first) {  // the rest of the first ring fill goes out behind the x loads
         trace_point(a, 8);
         first = false;
         if (lane == 0)
           for (int s = n_pre; s < n_first; ++s) issue(s);
       }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        if ((r0 + r) * T >= items) break;  // CTA-uniform
-        const int it = (r0 + r) * T + threadIdx.x;
-        const bool live = it < items;
-        const int sub = it & 7, st = (it >> 3) % nsteps, tk = live ? (it >> 3) / nsteps : 0;
-        const Digits d = digitize<IPU>(v[r], umask);
-        if (r0 + r == 0) trace_point(a, 11);
-        if (live) {
-          store_digits(bw, st, tk, TP, sub, d);
-          if ((it % IPU) == 0) xs[((it % (nsteps * 8)) / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
-        }
+      const Digits d = digitize<IPU>(v, umask);
+      if (it0 == 0) trace_point(a, 11);
+      if (live) {
+        store_digits(bw, st, tk, TP, sub, d);
+        if ((it % IPU) == 0) xs[((it % (nsteps * 8)) / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
       }
     }
     // zero fragments / unit params of the padding tokens M..TP-1
@@ -566,7 +542,8 @@ static int g_ring_kb = 0;     // tuning: ring bytes per CTA (KB; 0 = 10 KB per w
 static int g_max_ctas = 0;    // tuning: cap on the grid (0 = rule below)
 static int g_l2_self = 0;     // tuning: L2-prefetch each CTA's weights beyond the ring at entry
 static int g_pf_when = 1;
-static int g_max_split = kMaxSplits;  // tuning: cap on the cluster (K split) size     // tuning: when the next-kernel L2 hint is issued (0 entry, 1 after loop)
+static int g_max_split = kMaxSplits;
+static int g_carveout = -1;  // tuning: preferred shared-memory carveout (-1: driver default)  // tuning: cap on the cluster (K split) size     // tuning: when the next-kernel L2 hint is issued (0 entry, 1 after loop)
 static thread_local const void* t_pf_ptr[2] = {nullptr, nullptr};
 static thread_local int64_t t_pf_bytes[2] = {0, 0};
 
@@ -615,10 +592,13 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    // every kernel of a decode chain asks for the same (maximal) shared-memory
-    // carveout, so consecutive kernels can share an SM without a reconfiguration
-    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     configured = true;
+  }
+  static int carveout = -2;
+  if (carveout != g_carveout) {  // tuning aid: shared-memory carveout preference
+    carveout = g_carveout;
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        carveout));
   }
   const int stage = BITS * 512 + GPS * 128;
   auto shape = [&](int S) {  // smem plan for S chunks: ring of <= 80 KB per CTA
@@ -708,12 +688,6 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     pa.val.programmaticStreamSerializationAllowed = 1;
     pc.attrs = &pa;
     pc.numAttrs = 1;
-    static bool prep_configured = false;
-    if (!prep_configured) {
-      QIGEN_CUDA_RET(cudaFuncSetAttribute(act_prep_kernel<IPU>,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      prep_configured = true;
-    }
     QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_kernel<IPU>, a, (int)TP, (int)UPS));
   }
   cudaLaunchConfig_t cfg = {};
@@ -786,6 +760,11 @@ extern "C" int qigen_gemv_prefetch_next(const void* p0, int64_t bytes0, const vo
   t_pf_bytes[0] = p0 ? bytes0 : 0;
   t_pf_ptr[1] = p1;
   t_pf_bytes[1] = p1 ? bytes1 : 0;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_carveout(int pct) {
+  g_carveout = pct;
   return QIGEN_OK;
 }
 

@@ -54,6 +54,7 @@ constexpr int kGDepth = 2;             // weight stages per consumer warp
 constexpr int kRecSlot = kGSS * kRecBytes;
 constexpr int kGRecDepth = 4;          // activation-record stages in the CTA ring
 constexpr int kMaxSeq = 2048;          // items one CTA may claim (dynamic schedule)
+constexpr double kSplitPct = 20.0;     // K-split GEMVs with items below this % of the largest
 
 struct GDesc {
   const uint4* qw;
@@ -518,7 +519,9 @@ constexpr int kGSmem = kGWarps * kGDepth * kGSlot + kGRecDepth * kRecSlot +
 
 using namespace qigen;
 
-static int g_group_mode = 0;  // tuning: 1 stream only; 16 (at create) split K in two
+// tuning: 1 stream only; at create: 16 split every K in two, (pct+1) << 8 sets
+// the split threshold (1 << 8: never split)
+static int g_group_mode = 0;
 
 struct qigen_gemv_group {
   void* blob = nullptr;  // device: descs | items | cta_start
@@ -568,13 +571,30 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
             : e.group_size == 256 ? 1 : 0;
     d.M = (int)e.tokens;
     d.x_dtype = e.x_dtype;
-    // (tuning) split K in two halves when each keeps >= 4 supersteps: halves
-    // the item size and so the greedy schedule's tail, but costs more per-item
-    // overhead than it saves on the configs[1] sweep (measured), so it is off
-    d.split = (d.KS >= 8 && (g_group_mode & 16)) ? 1 : 0;
+    d.split = 0;  // decided below, once every GEMV's item cost is known
     d.rec0 = recs;
     recs += d.KS;
     max_ks = std::max(max_ks, d.KS);
+  }
+  // time model of an item per SM: max(stream at ~44 GB/s, issue at ~4.5
+  // instr/ns); ~110 warp instructions per panel superstep + ~17 per flush unit
+  auto item_cost = [](const GDesc& d, int act, int nks) {
+    const int zb = (d.gps > 0 ? d.gps : 1) * 128;
+    const int ups = d.gps > 2 ? d.gps : 2;
+    const double bytes = (double)nks * (act * (d.bits * 512 + zb) + kRecBytes);
+    const double instr = (double)nks * act * (110.0 + 17.0 * ups);
+    return std::max(bytes / 44.0, instr / 4.5);
+  };
+  // The greedy schedule's tail is about one of the last (cheapest) items: the
+  // GEMVs whose full-K items cost < kSplitPct % of the largest get their K
+  // split in two halves (each >= 4 supersteps); splitting everything costs
+  // more per-item overhead than it saves (measured).
+  {
+    double mx = 0.0;
+    for (const GDesc& d : ds) mx = std::max(mx, item_cost(d, kGWarps, d.KS));
+    const int pct_knob = (g_group_mode >> 8) & 0xff;
+    const double pct = (g_group_mode & 16) ? 101.0 : pct_knob ? pct_knob - 1 : kSplitPct;
+    for (GDesc& d : ds) d.split = (d.KS >= 8 && item_cost(d, kGWarps, d.KS) < mx * pct / 100.0);
   }
   // items (GEMV x 16 panels x K range) and their cost
   std::vector<GItem> items;
@@ -587,13 +607,7 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
       const int act = std::min(kGWarps, d.P - p0);
       const int k0 = hf * (d.KS / 2), k1 = halves == 1 || hf == 1 ? d.KS : d.KS / 2;
       items.push_back({i, p0, k0, k1});
-      // time model per SM: max(stream at ~44 GB/s, issue at ~4.5 instr/ns);
-      // ~110 warp instructions per panel superstep + ~17 per flush unit
-      const int zb = (d.gps > 0 ? d.gps : 1) * 128;
-      const int ups = d.gps > 2 ? d.gps : 2;
-      const double bytes = (double)(k1 - k0) * (act * (d.bits * 512 + zb) + kRecBytes);
-      const double instr = (double)(k1 - k0) * act * (110.0 + 17.0 * ups);
-      cost.push_back(std::max(bytes / 44.0, instr / 4.5));
+      cost.push_back(item_cost(d, act, k1 - k0));
     }
   }
   int dev = 0, sms = 148;

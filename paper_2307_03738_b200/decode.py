@@ -258,8 +258,9 @@ class LlamaTP:
                 cache[li] = g[:, self.h0:self.h1].to(kv_dtype)
                 del g
         self.attn_ws = backend.attention_workspace(batch, self.nh, hd, max_ctx, self.dev)
-        # L2 prefetch hints between consecutive GEMVs (GPU backend only)
-        self.l2_hints = backend is GpuBackend
+        # L2 prefetch hints between consecutive GEMVs: off (measured slower on
+        # the 7B chain, tools/decode_layer_exp.py); kept as an option
+        self.l2_hints = False
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device=self.dev).float() / hd))
         ang = torch.arange(max_ctx, device=self.dev).float()[:, None] * inv[None, :]
         self.cos, self.sin = ang.cos(), ang.sin()  # [ctx, hd/2]

@@ -13,8 +13,10 @@ ap.add_argument("--variants", default="0:0:8:0:0:0",
                 help="comma list of early:policy:wpc:ring_kb:max_ctas:splits")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--x-ready", type=int, default=0)
+ap.add_argument("--carveout", type=int, default=-1)
 args = ap.parse_args()
 L = _lib.lib()
+L.qigen_debug_carveout(args.carveout)
 dev = torch.device("cuda")
 for case in args.cases.split(","):
     shp, b, gs = case.split(":")

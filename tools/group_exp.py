@@ -19,7 +19,7 @@ for i, (b, g, (K, N)) in enumerate(SWEEP):
     yref.append(pw.gemv(x))
 import os
 from paper_2307_03738_b200 import _lib as _L
-_L.lib().qigen_debug_group_mode(int(os.environ.get("GMODE", "0")))
+_L.lib().qigen_debug_group_mode(int(os.environ.get("GMODE", "0"), 0))
 grp = GemvGroup(list(zip(pws, xs, ys)))
 _L.lib().qigen_debug_group_mode(0)
 grp.run(); torch.cuda.synchronize()
