@@ -89,14 +89,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Four consecutive activations of token tk (zero beyond n / for padding tokens).
 __device__ __forceinline__ void gload4(const GDesc& d, int tk, int64_t k, float (&v)[4]) {
+  const int64_t o = tk * d.ldx + k;
+  if (d.x_dtype == QIGEN_F32 && k + 3 < d.n && ((uintptr_t)((const float*)d.x + o) & 15) == 0) {
+    const float4 f = __ldg((const float4*)((const float*)d.x + o));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     float f = 0.f;
-    if (tk < d.M && k + i < d.n) {
-      const int64_t o = tk * d.ldx + k + i;
-      if (d.x_dtype == QIGEN_F32) f = __ldg((const float*)d.x + o);
-      else if (d.x_dtype == QIGEN_F16) f = __half2float(((const __half*)d.x)[o]);
-      else f = __bfloat162float(((const __nv_bfloat16*)d.x)[o]);
+    if (k + i < d.n) {
+      if (d.x_dtype == QIGEN_F32) f = __ldg((const float*)d.x + o + i);
+      else if (d.x_dtype == QIGEN_F16) f = __half2float(((const __half*)d.x)[o + i]);
+      else f = __bfloat162float(((const __nv_bfloat16*)d.x)[o + i]);
     }
     v[i] = f;
   }
@@ -112,6 +117,14 @@ __device__ __forceinline__ void group_prep_item(const GPlan& pl, const GDesc& d,
   unsigned char* rec = pl.rec + (size_t)(d.rec0 + (live ? sup : 0)) * kRecBytes;
 #pragma unroll
   for (int tk = 0; tk < kGTP; ++tk) {
+    if (tk >= d.M) {  // padding token (CTA-uniform): zero digits and flush factors
+      if (live) {
+        store_digits((uint32_t*)rec, sl, tk, kGTP, sub, Digits{{0u, 0u, 0u, 0u}, 0.f, 0.f});
+        if ((it % IPU) == 0)
+          ((float4*)(rec + kRecDig))[((it % 64) / IPU) * kGTP + tk] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
     float v[4] = {0.f, 0.f, 0.f, 0.f};
     if (live) gload4(d, tk, (int64_t)32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v);
     const Digits dg = digitize<IPU>(v, umask);
@@ -121,8 +134,7 @@ __device__ __forceinline__ void group_prep_item(const GPlan& pl, const GDesc& d,
         const int uj = (it % 64) / IPU;
         // dg.scale is a power of two: both products are exact
         ((float4*)(rec + kRecDig))[uj * kGTP + tk] =
-            tk < d.M ? make_float4(dg.scale * 65536.f, dg.xsum * dg.scale, dg.scale, 0.f)
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            make_float4(dg.scale * 65536.f, dg.xsum * dg.scale, dg.scale, 0.f);
       }
     }
   }
