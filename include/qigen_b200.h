@@ -132,12 +132,6 @@ int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, in
                   const float* prologue_w, float eps, void* workspace, int64_t workspace_bytes,
                   void* stream);
 
-/* One-shot hint for the NEXT qigen_gemv / qigen_gemv_ex launch on this host
- * thread: while it runs, its CTAs pull [p0, p0+bytes0) and [p1, p1+bytes1) (the
- * weights of the kernel that will follow it, e.g. the next layer's linear in a
- * decode step) into L2, so that kernel's weight stream starts from L2.  NULL /
- * 0 ranges are skipped; 16-byte aligned. */
-int qigen_gemv_prefetch_next(const void* p0, int64_t bytes0, const void* p1, int64_t bytes1);
 
 /* ---- grouped GEMV: many independent GEMVs in one persistent launch ----------
  * Replaces a sequence of independent qgemv(pm_i, x_i) calls of the reference
@@ -217,10 +211,6 @@ int qigen_debug_prefetch(int stages_before_wait);
 /* Tuning aid: 1 = always digitise activations in the separate prep kernel. */
 int qigen_debug_force_prep(int on);
 /* Tuning aid: 1 = trigger the dependent launch (PDL) at GEMV kernel entry. */
-/* Tuning aid: self = L2-prefetch each CTA's weights beyond its first ring fill at
- * entry; when = issue the qigen_gemv_prefetch_next hint at entry (0) or after the
- * main loop (1, default). */
-int qigen_debug_l2_prefetch(int self, int when);
 /* Tuning aid: cap the automatic K split (thread-block cluster size) of the GEMV. */
 int qigen_debug_max_split(int s);
 /* Tuning aid: preferred shared-memory carveout (percent, -1 = driver default) of the GEMV. */

@@ -52,10 +52,6 @@ struct GemvArgs {
   int x_vec;         // x rows 16-byte aligned -> vector loads
   int accumulate;
   int x_ready;       // x is not written by the preceding kernel: read it before the PDL wait
-  int l2_self;       // L2-prefetch this CTA's weights beyond the first ring fill at entry
-  const char* pf_ptr[2];  // L2 prefetch hint for the NEXT kernel's data (split over CTAs)
-  int64_t pf_bytes[2];
-  int pf_when;            // 0: at entry, 1: after the main loop
   int max_steps;     // max K-steps (32 rows) of any chunk
   int D;             // ring stages per warp
   int pre;           // stages per warp issued before griddepcontrol.wait
@@ -268,27 +264,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     for (int i = 0; i < D; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < n_pre; ++s) issue(s);
-    if (a.l2_self && nks > n_first) {
-      // the rest of this warp's chunk streams into L2 now, so the ring refills
-      // after the PDL wait hit L2 instead of waiting on DRAM
-      bulk_prefetch_l2(wsrc + (int64_t)(ks0 + n_first) * BITS * 512,
-                       (uint32_t)((nks - n_first) * BITS * 512));
-      if (SZB) bulk_prefetch_l2(zsrc + (int64_t)(ks0 + n_first) * SZB, (uint32_t)((nks - n_first) * SZB));
-    }
   }
-  auto prefetch_next = [&]() {  // this CTA's slice of the next kernel's data
-    if (threadIdx.x != 0) return;
-    const int64_t nctas = (int64_t)gridDim.x * gridDim.y;
-    const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-    for (int r = 0; r < 2; ++r) {
-      if (!a.pf_ptr[r] || a.pf_bytes[r] <= 0) continue;
-      const int64_t per = ((a.pf_bytes[r] + nctas - 1) / nctas + 15) / 16 * 16;
-      const int64_t b0 = cta * per, b1 = min(a.pf_bytes[r], b0 + per);
-      for (int64_t o = b0; o < b1; o += 65536)
-        bulk_prefetch_l2(a.pf_ptr[r] + o, (uint32_t)min((int64_t)65536, b1 - o));
-    }
-  };
-  if (a.pf_when == 0) prefetch_next();
   if (threadIdx.x < 2) ((uint32_t*)(smem + L.zero))[threadIdx.x] = 0u;
   uint64_t* rbar = (uint64_t*)(smem + L.rbar);
   uint64_t* pbar = (uint64_t*)(smem + L.pbar);
@@ -487,7 +463,6 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     }
   }
   trace_point(a, 3);
-  if (a.pf_when == 1) prefetch_next();
 
   // ---- 5. combine digit-pair lanes; deterministic split-K reduction ---------
   // Element e = (warp*16 + row)*M + token of this CTA column.  With S > 1 the
@@ -540,12 +515,8 @@ static int g_policy = 0;      // tuning: L2 evict_first hint on weight copies
 static int g_wpc = 8;         // tuning: warps per CTA for <= 4 tokens (8 or 16)
 static int g_ring_kb = 0;     // tuning: ring bytes per CTA (KB; 0 = 10 KB per warp)
 static int g_max_ctas = 0;    // tuning: cap on the grid (0 = rule below)
-static int g_l2_self = 0;     // tuning: L2-prefetch each CTA's weights beyond the ring at entry
-static int g_pf_when = 1;
-static int g_max_split = kMaxSplits;
-static int g_carveout = -1;  // tuning: preferred shared-memory carveout (-1: driver default)  // tuning: cap on the cluster (K split) size     // tuning: when the next-kernel L2 hint is issued (0 entry, 1 after loop)
-static thread_local const void* t_pf_ptr[2] = {nullptr, nullptr};
-static thread_local int64_t t_pf_bytes[2] = {0, 0};
+static int g_max_split = kMaxSplits;  // tuning: cap on the automatic K split (cluster size)
+static int g_carveout = -1;           // tuning: preferred shared-memory carveout (-1: default)
 
 static int sm_count() {
   static int cached = 0;
@@ -751,18 +722,6 @@ extern "C" int qigen_debug_prefetch(int stages_before_wait) {
   return QIGEN_OK;
 }
 
-extern "C" int qigen_gemv_prefetch_next(const void* p0, int64_t bytes0, const void* p1,
-                                        int64_t bytes1) {
-  QIGEN_CHECK_ARG(bytes0 >= 0 && bytes1 >= 0 && (bytes0 % 16) == 0 && (bytes1 % 16) == 0 &&
-                      ((uintptr_t)p0 % 16) == 0 && ((uintptr_t)p1 % 16) == 0,
-                  QIGEN_ERR_ARG, "prefetch ranges must be 16-byte aligned and sized");
-  t_pf_ptr[0] = p0;
-  t_pf_bytes[0] = p0 ? bytes0 : 0;
-  t_pf_ptr[1] = p1;
-  t_pf_bytes[1] = p1 ? bytes1 : 0;
-  return QIGEN_OK;
-}
-
 extern "C" int qigen_debug_carveout(int pct) {
   g_carveout = pct;
   return QIGEN_OK;
@@ -770,12 +729,6 @@ extern "C" int qigen_debug_carveout(int pct) {
 
 extern "C" int qigen_debug_max_split(int s) {
   g_max_split = s < 1 ? 1 : (s > kMaxSplits ? kMaxSplits : s);
-  return QIGEN_OK;
-}
-
-extern "C" int qigen_debug_l2_prefetch(int self, int when) {
-  g_l2_self = self;
-  g_pf_when = when;
   return QIGEN_OK;
 }
 
@@ -856,14 +809,6 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   a.x_ready = (accumulate & QIGEN_GEMV_X_READY) ? 1 : 0;
   a.trace = g_trace;
   a.trace_clk = g_trace_clk;
-  a.l2_self = g_l2_self;
-  a.pf_when = g_pf_when;
-  for (int r = 0; r < 2; ++r) {  // consume the one-shot hint of qigen_gemv_prefetch_next
-    a.pf_ptr[r] = (const char*)t_pf_ptr[r];
-    a.pf_bytes[r] = t_pf_bytes[r];
-    t_pf_ptr[r] = nullptr;
-    t_pf_bytes[r] = 0;
-  }
   a.early = g_early || a.x_ready;  // independent x: overlap the predecessor fully
   a.policy = g_policy;
   const int S = k_splits;  // 0: chosen per launch shape in launch_cfg

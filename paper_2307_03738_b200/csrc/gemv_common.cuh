@@ -51,11 +51,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       : "memory");
 }
 
-// Pull [src, src + bytes) into L2 (no shared-memory destination); bytes % 16 == 0.
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
 // Cluster address of the same shared-memory offset in CTA `rank`.
 __device__ __forceinline__ uint32_t mapa(const void* p, int rank) {
   uint32_t r;

@@ -141,11 +141,9 @@ class GpuLinear:
         self.K, self.N = w.shape
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,
-                 prologue: str | None = None, norm_weight=None, eps: float = 1e-5,
-                 prefetch: "GpuLinear | None" = None) -> torch.Tensor:
+                 prologue: str | None = None, norm_weight=None, eps: float = 1e-5) -> torch.Tensor:
         return self.pw.gemv(x, out=out, accumulate=accumulate, prologue=prologue,
-                            norm_weight=norm_weight, eps=eps,
-                            prefetch=prefetch.pw if prefetch is not None else None)
+                            norm_weight=norm_weight, eps=eps)
 
     @property
     def nbytes(self) -> int:
@@ -258,9 +256,6 @@ class LlamaTP:
                 cache[li] = g[:, self.h0:self.h1].to(kv_dtype)
                 del g
         self.attn_ws = backend.attention_workspace(batch, self.nh, hd, max_ctx, self.dev)
-        # L2 prefetch hints between consecutive GEMVs: off (measured slower on
-        # the 7B chain, tools/decode_layer_exp.py); kept as an option
-        self.l2_hints = False
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device=self.dev).float() / hd))
         ang = torch.arange(max_ctx, device=self.dev).float()[:, None] * inv[None, :]
         self.cos, self.sin = ang.cos(), ang.sin()  # [ctx, hd/2]
@@ -288,20 +283,14 @@ class LlamaTP:
         cos, sin = self.cos[pos], self.sin[pos]
         scale = 1.0 / math.sqrt(hd)
         att = torch.empty((B, self.nh * hd), dtype=torch.float32, device=self.dev)
-        # each GEMV pulls the next GEMV's weights into L2 while it runs
-        pf = self.l2_hints
         for li, lay in enumerate(self.layers):
-            nxt = self.layers[li + 1]["qkv"] if li + 1 < len(self.layers) else None
-            qkv = lay["qkv"](h, prologue="rmsnorm", norm_weight=lay["n1"], eps=cfg.norm_eps,
-                             **({"prefetch": lay["o"]} if pf else {}))
+            qkv = lay["qkv"](h, prologue="rmsnorm", norm_weight=lay["n1"], eps=cfg.norm_eps)
             # RoPE + KV append + attention over positions 0..pos
             be.attention(qkv, cos, sin, self.k_cache[li], self.v_cache[li], pos, scale, att,
                          self.attn_ws)
-            h = self._row_parallel(lay["o"], att, h, prefetch=lay["gu"] if pf else None)
-            gu = lay["gu"](h, prologue="rmsnorm", norm_weight=lay["n2"], eps=cfg.norm_eps,
-                           **({"prefetch": lay["down"]} if pf else {}))
-            h = self._row_parallel(lay["down"], gu, h, prologue="swiglu",
-                                   prefetch=nxt if pf else None)
+            h = self._row_parallel(lay["o"], att, h)
+            gu = lay["gu"](h, prologue="rmsnorm", norm_weight=lay["n2"], eps=cfg.norm_eps)
+            h = self._row_parallel(lay["down"], gu, h, prologue="swiglu")
         xn = torch.empty((B, cfg.d_model), dtype=torch.float16, device=self.dev)
         be.rmsnorm_f16(h, self.norm, cfg.norm_eps, xn)
         logits = (xn @ self.lm_head.t()).float()           # [B, V_l]
@@ -309,17 +298,15 @@ class LlamaTP:
         self.last_logits = logits
         return logits.argmax(-1)
 
-    def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor, prologue=None,
-                      prefetch=None) -> torch.Tensor:
+    def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor, prologue=None) -> torch.Tensor:
         """Row-parallel linear + residual: rank 0 accumulates its partial into h
         inside the GEMV epilogue, the other ranks produce bare partials, and one
         all-reduce forms h + sum of partials on every rank."""
-        kw = {"prefetch": prefetch} if prefetch is not None else {}
         if self.tp.rank == 0:
-            lin(x, out=h, accumulate=True, prologue=prologue, **kw)
+            lin(x, out=h, accumulate=True, prologue=prologue)
             out = h
         else:
-            out = lin(x, prologue=prologue, **kw)
+            out = lin(x, prologue=prologue)
         return self.tp.all_reduce(out)
 
 

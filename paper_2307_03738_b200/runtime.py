@@ -156,12 +156,8 @@ class PanelWeights:
 
     def gemv(self, x: torch.Tensor, out: torch.Tensor | None = None, *, accumulate: bool = False,
              k_splits: int = 0, prologue: str | None = None, norm_weight: torch.Tensor | None = None,
-             eps: float = 1e-5, x_ready: bool = False,
-             prefetch: "PanelWeights | None" = None) -> torch.Tensor:
+             eps: float = 1e-5, x_ready: bool = False) -> torch.Tensor:
         """y[t, :] = f(x[t, :]) @ W for t < tokens; x: CUDA [tokens, n] or [n].
-
-        ``prefetch``: the weights of the GEMV that will run next on this stream;
-        this launch pulls them into L2 (qigen_gemv_prefetch_next).
 
         ``prologue`` fuses the producer-side glue into the GEMV: None (f = id),
         ``"rmsnorm"`` (f = RMSNorm with ``norm_weight``) or ``"swiglu"`` (x holds
@@ -204,9 +200,6 @@ class PanelWeights:
                      ws.data_ptr(), ws.numel(), st)
             return out.reshape(self.m) if squeeze else out
         ws = self._workspace(min(T, MAX_GEMV_TOKENS), x2.device)
-        if prefetch is not None:
-            call("qigen_gemv_prefetch_next", prefetch.qw.data_ptr(), prefetch.qw.numel() * 4,
-                 prefetch.qsz.data_ptr(), prefetch.qsz.numel() * 4)
         for t0 in range(0, T, MAX_GEMV_TOKENS):
             t1 = min(T, t0 + MAX_GEMV_TOKENS)
             xs, ys = x2[t0:t1], y2[t0:t1]

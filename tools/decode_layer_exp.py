@@ -22,8 +22,7 @@ gus = [torch.empty(1, 2 * cfg.ffn, device="cuda") for _ in range(L)]
 
 def full(pf=False):
     for li, lay in enumerate(m.layers):
-        nx = m.layers[(li + 1) % L]["qkv"]
-        k = (lambda t: {"prefetch": t}) if pf else (lambda t: {})
+        k = (lambda t: {})
         lay["qkv"](h, out=qkvs[li], prologue="rmsnorm", norm_weight=lay["n1"], **k(lay["o"]))
         be.attention(qkvs[li], cos, sin, m.k_cache[li], m.v_cache[li], pos, 1 / math.sqrt(128), att, m.attn_ws)
         lay["o"](att, out=h, accumulate=True, **k(lay["gu"]))
@@ -57,7 +56,7 @@ import os
 Lb = _lib.lib()
 s = torch.cuda.Stream()
 def base():
-    Lb.qigen_debug_l2_prefetch(0, 1); full(pf=False)
+    full(pf=False)
 variants = [("full layer", base)]
 for ms in [1, 2, 3, 4, 8]:
     def f(ms=ms):
@@ -65,8 +64,6 @@ for ms in [1, 2, 3, 4, 8]:
         full(pf=False)
         Lb.qigen_debug_max_split(16)
     variants.append((f"max split {ms}", f))
-def reset():
-    Lb.qigen_debug_l2_prefetch(0, 1)
 if os.environ.get("ALL"):
   variants += [("4 gemvs", gemvs),
                  ("qkv (rmsnorm)", one("qkv", prologue="rmsnorm", norm_weight=m.layers[0]["n1"])),
