@@ -58,6 +58,11 @@ s = torch.cuda.Stream()
 def base():
     full(pf=False)
 variants = [("full layer", base)]
+def early():
+    Lb.qigen_debug_early_trigger(1)
+    full(pf=False)
+    Lb.qigen_debug_early_trigger(0)
+variants.append(("early trigger", early))
 for ms in [1, 2, 3, 4, 8]:
     def f(ms=ms):
         Lb.qigen_debug_max_split(ms)

@@ -22,6 +22,7 @@ gus = [torch.empty(1, 2 * cfg.ffn, device="cuda") for _ in range(L)]
 Lb = _lib.lib()
 import os
 Lb.qigen_debug_prefetch(int(os.environ.get('PRE', '-1')))
+Lb.qigen_debug_early_trigger(int(os.environ.get('EARLY', '0')))
 bufs = {}
 
 
