@@ -22,12 +22,11 @@ gus = [torch.empty(1, 2 * cfg.ffn, device="cuda") for _ in range(L)]
 
 def full(pf=False):
     for li, lay in enumerate(m.layers):
-        k = (lambda t: {})
-        lay["qkv"](h, out=qkvs[li], prologue="rmsnorm", norm_weight=lay["n1"], **k(lay["o"]))
+        lay["qkv"](h, out=qkvs[li], prologue="rmsnorm", norm_weight=lay["n1"])
         be.attention(qkvs[li], cos, sin, m.k_cache[li], m.v_cache[li], pos, 1 / math.sqrt(128), att, m.attn_ws)
-        lay["o"](att, out=h, accumulate=True, **k(lay["gu"]))
-        lay["gu"](h, out=gus[li], prologue="rmsnorm", norm_weight=lay["n2"], **k(lay["down"]))
-        lay["down"](gus[li], out=h, accumulate=True, prologue="swiglu", **k(nx))
+        lay["o"](att, out=h, accumulate=True)
+        lay["gu"](h, out=gus[li], prologue="rmsnorm", norm_weight=lay["n2"])
+        lay["down"](gus[li], out=h, accumulate=True, prologue="swiglu")
 
 
 def gemvs():
