@@ -18,4 +18,7 @@ from .packing import (Layout, PackedMatrix, PackError, block_order, extract_code
 from .runtime import (GemvGroup, InputSums, PanelWeights, input_sums, memory_report, qgemv,
                       qgemv_batch, qgemv_reference)
 
+from .weightfile import (BadMagicError, ChecksumError, TruncatedError, VersionError,
+                         WeightFileError, load_panels, read_weight_file, write_weight_file)
+
 __version__ = "0.1.0"
