@@ -8,6 +8,10 @@
 #include "common.cuh"
 #include "gemv_common.cuh"
 
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
 namespace qigen {
 
 // qkv: f32 [B, 3, H, hd] (the fused QKV GEMV output).  Rotates q and k at
@@ -73,14 +77,16 @@ __global__ void __launch_bounds__(1024) rmsnorm_f16_kernel(const float* __restri
 
 // ---- fused decode attention ---------------------------------------------------
 // One new token per sequence attends over its KV cache (flash-decoding split
-// over positions).  Per CTA: one (sequence, head) and a chunk of kAttnChunk
-// positions.  The chunk's cached K/V rows (written by earlier decode steps, not
-// by the preceding kernel) are bulk-copied into shared memory BEFORE the PDL
-// wait, so they stream while the QKV GEMV finishes; after the wait the CTA
-// applies RoPE to q (and, in the chunk holding `pos`, to the new k, appending
-// k/v to the cache), computes its partial softmax state, and the last CTA of
-// the head combines the partials in split order (deterministic).
-constexpr int kAttnChunk = 64;
+// over positions).  Per CTA: one (sequence, head) and a chunk of positions; the
+// nsplit CTAs of a head form a thread-block cluster (nsplit <= 16).  The
+// chunk's cached K/V rows (written by earlier decode steps, not by the
+// preceding kernel) are bulk-copied into shared memory BEFORE the PDL wait, so
+// they stream while the QKV GEMV finishes; after the wait the CTA applies RoPE
+// to q (and, in the chunk holding `pos`, to the new k, appending k/v to the
+// cache) and computes its partial softmax state (m, l, acc), which it writes
+// into the rank-0 CTA's shared memory (DSMEM); after one cluster barrier rank 0
+// combines the partials in split order (deterministic, no global round trip).
+constexpr int kAttnMaxSplit = 16;
 
 struct AttnArgs {
   const float* qkv;  // [B, 3, H, HD] f32 (the fused QKV GEMV output)
@@ -88,10 +94,8 @@ struct AttnArgs {
   const float* sinv;  // [HD/2] at pos
   __half* kc;
   __half* vc;  // [B, H, ctx, HD]
-  float* part;  // [B*H][nsplit][HD + 2] partial (acc, m, l)
-  int* cnt;     // [B*H] arrival counters (left at 0)
-  float* out;   // [B, H * HD]
-  int B, H, ctx, pos, nsplit;
+  float* out;  // [B, H * HD]
+  int B, H, ctx, pos, nsplit, chunk;
   float scale;
   unsigned long long* trace;  // optional per-CTA %globaltimer: entry, after wait, exit
 };
@@ -104,21 +108,25 @@ __device__ __forceinline__ void attn_trace(const AttnArgs& a, int i) {
   }
 }
 
+// dynamic shared memory: K chunk | V chunk (f16 [chunk][HD] each) | scores
+// [chunk] | inbox [kAttnMaxSplit][HD + 2] (rank 0: every split's acc, m, l)
 template <int HD>
 __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
-  __shared__ __align__(128) __half ks[kAttnChunk * HD];
-  __shared__ __align__(128) __half vs[kAttnChunk * HD];
+  extern __shared__ __align__(128) unsigned char sm[];
+  __half* ks = (__half*)sm;
+  __half* vs = ks + a.chunk * HD;
+  float* ps = (float*)(vs + a.chunk * HD);
+  float* inbox = ps + a.chunk;
   __shared__ float qs[HD];
-  __shared__ float ps[kAttnChunk];
   __shared__ float red[2];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int last;
-  const int split = blockIdx.x, bh = blockIdx.y;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int split = blockIdx.x, bh = blockIdx.y;  // cluster rank == split
   const int b = bh / a.H, h = bh % a.H;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int p0 = split * kAttnChunk;
-  const int p1 = min(p0 + kAttnChunk, a.pos + 1);  // positions [p0, p1)
-  const int pe = min(p1, a.pos);                    // cached rows [p0, pe)
+  const int p0 = split * a.chunk;
+  const int p1 = min(p0 + a.chunk, a.pos + 1);  // positions [p0, p1)
+  const int pe = min(p1, a.pos);                // cached rows [p0, pe)
   attn_trace(a, 0);
   asm volatile("griddepcontrol.launch_dependents;");
   const size_t row0 = ((size_t)bh * a.ctx + p0) * HD;
@@ -139,7 +147,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   const float* k = a.qkv + ((size_t)(b * 3 + 1) * a.H + h) * HD;
   const float* v = a.qkv + ((size_t)(b * 3 + 2) * a.H + h) * HD;
   constexpr int half = HD / 2;
-  const bool mine = a.pos >= p0 && a.pos < p0 + kAttnChunk;  // this chunk holds the new token
+  const bool mine = a.pos >= p0 && a.pos < p0 + a.chunk;  // this chunk holds the new token
   for (int i = tid; i < half; i += blockDim.x) {
     const float c = a.cosv[i], s = a.sinv[i];
     // rotate-half with separately rounded products (no FMA contraction: the
@@ -198,44 +206,31 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
     }
   }
   __syncthreads();
-  float* pp = a.part + ((size_t)bh * a.nsplit + split) * (HD + 2);
+  // partial state into the rank-0 CTA's inbox (distributed shared memory)
+  float* dst = cluster.map_shared_rank(inbox, 0) + split * (HD + 2);
   for (int d = tid; d < HD; d += blockDim.x) {
     float acc = 0.f;
     for (int j = 0; j < n; ++j) acc += ps[j] * __half2float(vs[j * HD + d]);
-    pp[d] = acc;
+    dst[d] = acc;
   }
   if (tid == 0) {
-    pp[HD] = red[0];
-    pp[HD + 1] = red[1];
+    dst[HD] = red[0];
+    dst[HD + 1] = red[1];
   }
-  // the last CTA of this (sequence, head) combines the partials in split order
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) last = atomicAdd(&a.cnt[bh], 1) == a.nsplit - 1;
-  __syncthreads();
   attn_trace(a, 2);
-  if (!last) return;
-  __threadfence();
-  // all partials in one round trip: (m, l) of every split into shared memory,
-  // then each thread its dimension of every split (independent loads)
-  const float* P = a.part + (size_t)bh * a.nsplit * (HD + 2);
-  float* msh = ps;  // reuse: [nsplit] weights exp(m_s - M) (nsplit <= kAttnChunk here)
-  __shared__ float lsh[kAttnChunk];
-  for (int s = tid; s < a.nsplit; s += blockDim.x) {
-    msh[s] = __ldcg(P + s * (HD + 2) + HD);
-    lsh[s] = __ldcg(P + s * (HD + 2) + HD + 1);
-  }
-  __syncthreads();
+  cluster.sync();  // release the partials / acquire them in rank 0
+  if (split != 0) return;
+  // rank 0: combine in split order
   if (warp == 0) {
     float M = -INFINITY;
-    for (int s = lane; s < a.nsplit; s += 32) M = fmaxf(M, msh[s]);
+    for (int s = lane; s < a.nsplit; s += 32) M = fmaxf(M, inbox[s * (HD + 2) + HD]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.f;
     for (int s = lane; s < a.nsplit; s += 32) {
-      const float e = __expf(msh[s] - M);
-      msh[s] = e;
-      L += e * lsh[s];
+      const float e = __expf(inbox[s * (HD + 2) + HD] - M);
+      ps[s] = e;  // the weights of the splits (rank 0's scores are no longer needed)
+      L += e * inbox[s * (HD + 2) + HD + 1];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
@@ -245,10 +240,9 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   const float inv = red[1];
   for (int d = tid; d < HD; d += blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < a.nsplit; ++s) acc += msh[s] * __ldcg(P + s * (HD + 2) + d);
+    for (int s = 0; s < a.nsplit; ++s) acc += ps[s] * inbox[s * (HD + 2) + d];
     a.out[(size_t)b * a.H * HD + h * HD + d] = acc * inv;
   }
-  if (tid == 0) a.cnt[bh] = 0;
   attn_trace(a, 3);
 }
 
@@ -264,24 +258,29 @@ extern "C" int qigen_debug_attn_trace(void* buf) {
 
 extern "C" int64_t qigen_attn_decode_workspace_size(int64_t batch, int64_t heads, int64_t head_dim,
                                                     int64_t ctx) {
-  const int64_t nsplit = (ctx + kAttnChunk - 1) / kAttnChunk;
-  return batch * heads * (nsplit * (head_dim + 2) * 4 + 4) + 256;
+  (void)batch; (void)heads; (void)head_dim; (void)ctx;
+  return 0;  // the split partials are combined on chip (cluster shared memory)
 }
 
 extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
                                  const float* cos_pos, const float* sin_pos, void* k_cache,
                                  void* v_cache, int64_t ctx, int64_t pos, float scale, float* out,
                                  void* workspace, int64_t workspace_bytes, void* stream) {
-  QIGEN_CHECK_ARG(qkv && cos_pos && sin_pos && k_cache && v_cache && out && workspace,
-                  QIGEN_ERR_ARG, "null pointer");
+  (void)workspace; (void)workspace_bytes;
+  QIGEN_CHECK_ARG(qkv && cos_pos && sin_pos && k_cache && v_cache && out, QIGEN_ERR_ARG,
+                  "null pointer");
   QIGEN_CHECK_ARG(head_dim == 64 || head_dim == 128, QIGEN_ERR_UNSUPPORTED,
                   "decode attention takes head_dim 64 or 128, got %lld", (long long)head_dim);
-  QIGEN_CHECK_ARG(pos >= 0 && pos < ctx && batch > 0 && heads > 0, QIGEN_ERR_ARG,
-                  "bad position / shape");
-  QIGEN_CHECK_ARG((pos + kAttnChunk) / kAttnChunk <= kAttnChunk, QIGEN_ERR_UNSUPPORTED,
-                  "decode attention supports up to %d positions", kAttnChunk * kAttnChunk);
-  QIGEN_CHECK_ARG(workspace_bytes >= qigen_attn_decode_workspace_size(batch, heads, head_dim, ctx),
-                  QIGEN_ERR_ARG, "attention workspace too small");
+  QIGEN_CHECK_ARG(pos >= 0 && pos < ctx && batch > 0 && heads > 0 && batch * heads < 65536,
+                  QIGEN_ERR_ARG, "bad position / shape");
+  // chunk: a multiple of 64 positions, at most kAttnMaxSplit chunks (one cluster)
+  const int64_t npos = pos + 1;
+  int64_t chunk = 64;
+  while ((npos + chunk - 1) / chunk > kAttnMaxSplit) chunk += 64;
+  const size_t smem = (size_t)chunk * head_dim * 2 * 2 + chunk * 4 +
+                      (size_t)kAttnMaxSplit * (head_dim + 2) * 4;
+  QIGEN_CHECK_ARG(smem <= 200 * 1024, QIGEN_ERR_UNSUPPORTED,
+                  "decode attention: %lld positions do not fit one cluster", (long long)npos);
   AttnArgs a;
   a.qkv = qkv;
   a.cosv = cos_pos;
@@ -292,24 +291,36 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
   a.H = (int)heads;
   a.ctx = (int)ctx;
   a.pos = (int)pos;
-  a.nsplit = (int)((pos + 1 + kAttnChunk - 1) / kAttnChunk);
+  a.chunk = (int)chunk;
+  a.nsplit = (int)((npos + chunk - 1) / chunk);
   a.scale = scale;
   a.out = out;
   a.trace = g_attn_trace;
-  // counters first (zero-initialised by the caller, left at zero by the kernel)
-  a.cnt = (int*)workspace;
-  a.part = (float*)((char*)workspace + ((batch * heads * 4 + 255) / 256) * 256);
+  auto kern = head_dim == 128 ? attn_decode_kernel<128> : attn_decode_kernel<64>;
+  static bool configured = false;
+  if (!configured) {
+    for (auto kf : {attn_decode_kernel<128>, attn_decode_kernel<64>}) {
+      QIGEN_CUDA_RET(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024));
+      QIGEN_CUDA_RET(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    configured = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)a.nsplit, (unsigned)(batch * heads), 1);
   cfg.blockDim = dim3(128, 1, 1);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute pa;
-  pa.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  pa.val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = &pa;
-  cfg.numAttrs = 1;
-  if (head_dim == 128) QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<128>, a));
-  else QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, attn_decode_kernel<64>, a));
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = (unsigned)a.nsplit;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, kern, a));
   return QIGEN_OK;
 }
 
