@@ -215,6 +215,9 @@ int qigen_debug_force_prep(int on);
 int qigen_debug_max_split(int s);
 /* Tuning aid: preferred shared-memory carveout (percent, -1 = driver default) of the GEMV. */
 int qigen_debug_carveout(int pct);
+/* Tuning aid: 1 (default) = GEMVs with the RMSNorm prologue digitise through the
+ * one-CTA-per-token prep kernel. */
+int qigen_debug_norm_prep(int on);
 /* Tuning aid: L2 evict_first on weight copies, warps per CTA (8/16), ring KB per CTA, grid cap. */
 int qigen_debug_gemv_tuning(int policy, int wpc, int ring_kb, int max_ctas);
 int qigen_debug_early_trigger(int on);
@@ -225,6 +228,8 @@ int qigen_debug_group_mode(int mode);
 /* Debugging aid: per-CTA %globaltimer stamps of the decode attention kernel
  * (entry, after the PDL wait, before the combine, exit) at buf[cta * 4 + i]. */
 int qigen_debug_attn_trace(void* buf);
+/* Tuning aid: cap on the position splits (cluster size, <= 16) per head of the decode attention. */
+int qigen_debug_attn_splits(int n);
 
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
 

@@ -60,6 +60,7 @@ SIGNATURES = {
                              _I32, _I32, _I32, _P, ctypes.c_float, _P, _I64, _P]),
     "qigen_debug_max_split": (_I32, [_I32]),
     "qigen_debug_carveout": (_I32, [_I32]),
+    "qigen_debug_norm_prep": (_I32, [_I32]),
     "qigen_gemv_group_create": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
     "qigen_gemv_group_run": (_I32, [_P, _P]),
     "qigen_gemv_group_destroy": (_I32, [_P]),
@@ -80,6 +81,7 @@ SIGNATURES = {
     "qigen_debug_tc_mode": (_I32, [_I32]),
     "qigen_debug_group_mode": (_I32, [_I32]),
     "qigen_debug_attn_trace": (_I32, [_P]),
+    "qigen_debug_attn_splits": (_I32, [_I32]),
     "qigen_weights_create": (_I32, [_P, _I32, _I64, _I64, _I32, _I64, _I64, _I64, _P, _I64,
                                     _P, _P, _P, ctypes.POINTER(_P)]),
     "qigen_weights_destroy": (_I32, [_P]),

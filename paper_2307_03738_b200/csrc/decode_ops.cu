@@ -5,6 +5,8 @@
 // the attention itself, and the final RMSNorm before the fp16 lm_head.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "gemv_common.cuh"
 
@@ -175,16 +177,37 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   }
   if (pe > p0) mbar_wait(&bar, 0);
   __syncthreads();
-  // scores: a warp per position, lanes over the head dimension
+  // scores: a warp per position (4 positions per pass for ILP), lanes over
+  // the head dimension with vector loads of K
   const int n = p1 - p0;
-  constexpr int DPL = HD / 32;  // dims per lane
-  for (int j = warp; j < n; j += blockDim.x / 32) {
-    float acc = 0.f;
+  constexpr int DPL = HD / 32;  // dims per lane (4 or 2)
+  float qv[DPL];
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) acc += qs[lane * DPL + e] * __half2float(ks[j * HD + lane * DPL + e]);
+  for (int e = 0; e < DPL; ++e) qv[e] = qs[lane * DPL + e];
+  for (int j0 = warp * 4; j0 < n; j0 += (blockDim.x / 32) * 4) {
+    float acc[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) ps[j] = acc * a.scale;
+    for (int u = 0; u < 4; ++u) {
+      acc[u] = 0.f;
+      const int j = j0 + u;
+      if (j < n) {
+        const __half* kr = ks + j * HD + lane * DPL;
+        if constexpr (DPL == 4) {
+          const uint2 raw = *(const uint2*)kr;
+          const float2 k01 = __half22float2(*(const __half2*)&raw.x);
+          const float2 k23 = __half22float2(*(const __half2*)&raw.y);
+          acc[u] = qv[0] * k01.x + qv[1] * k01.y + qv[2] * k23.x + qv[3] * k23.y;
+        } else {
+          const float2 k01 = __half22float2(*(const __half2*)kr);
+          acc[u] = qv[0] * k01.x + qv[1] * k01.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+    if (lane < 4 && j0 + lane < n) ps[j0 + lane] = (lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3]) * a.scale;
   }
   __syncthreads();
   if (warp == 0) {
@@ -206,12 +229,33 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
     }
   }
   __syncthreads();
-  // partial state into the rank-0 CTA's inbox (distributed shared memory)
+  // P V: thread = (dim pair, position residue class); half2 loads of V, the
+  // NPH classes summed in fixed order; the partial state goes into the rank-0
+  // CTA's inbox (distributed shared memory)
+  constexpr int NPAIR = HD / 2, NPH = 128 / NPAIR;  // 64 pairs x 2 or 32 x 4
+  __shared__ float2 pv[128];
+  {
+    const int dp = tid % NPAIR, ph = tid / NPAIR;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int j = ph; j < n; j += NPH) {
+      const float2 vv = __half22float2(*(const __half2*)(vs + j * HD + 2 * dp));
+      const float w = ps[j];
+      acc.x = fmaf(w, vv.x, acc.x);
+      acc.y = fmaf(w, vv.y, acc.y);
+    }
+    pv[tid] = acc;
+  }
+  __syncthreads();
   float* dst = cluster.map_shared_rank(inbox, 0) + split * (HD + 2);
-  for (int d = tid; d < HD; d += blockDim.x) {
-    float acc = 0.f;
-    for (int j = 0; j < n; ++j) acc += ps[j] * __half2float(vs[j * HD + d]);
-    dst[d] = acc;
+  if (tid < NPAIR) {
+    float2 t = pv[tid];
+#pragma unroll
+    for (int q = 1; q < NPH; ++q) {
+      t.x += pv[q * NPAIR + tid].x;
+      t.y += pv[q * NPAIR + tid].y;
+    }
+    dst[2 * tid] = t.x;
+    dst[2 * tid + 1] = t.y;
   }
   if (tid == 0) {
     dst[HD] = red[0];
@@ -251,6 +295,11 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
 using namespace qigen;
 
 static unsigned long long* g_attn_trace = nullptr;
+static int g_attn_splits = 12;  // splits (cluster size) cap per head: 12 measured best at ctx 1025 (tools/attn_exp.py)
+extern "C" int qigen_debug_attn_splits(int n) {
+  g_attn_splits = n < 1 ? 1 : (n > kAttnMaxSplit ? kAttnMaxSplit : n);
+  return QIGEN_OK;
+}
 extern "C" int qigen_debug_attn_trace(void* buf) {
   g_attn_trace = (unsigned long long*)buf;
   return QIGEN_OK;
@@ -273,10 +322,10 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
                   "decode attention takes head_dim 64 or 128, got %lld", (long long)head_dim);
   QIGEN_CHECK_ARG(pos >= 0 && pos < ctx && batch > 0 && heads > 0 && batch * heads < 65536,
                   QIGEN_ERR_ARG, "bad position / shape");
-  // chunk: a multiple of 64 positions, at most kAttnMaxSplit chunks (one cluster)
+  // chunk: >= 64 positions (a multiple of 8), at most kAttnMaxSplit chunks (one
+  // cluster); long contexts get just enough positions per CTA to fit
   const int64_t npos = pos + 1;
-  int64_t chunk = 64;
-  while ((npos + chunk - 1) / chunk > kAttnMaxSplit) chunk += 64;
+  int64_t chunk = std::max<int64_t>(64, ((npos + g_attn_splits - 1) / g_attn_splits + 7) / 8 * 8);
   const size_t smem = (size_t)chunk * head_dim * 2 * 2 + chunk * 4 +
                       (size_t)kAttnMaxSplit * (head_dim + 2) * 4;
   QIGEN_CHECK_ARG(smem <= 200 * 1024, QIGEN_ERR_UNSUPPORTED,

@@ -186,6 +186,72 @@ __global__ void __launch_bounds__(256) act_prep_kernel(const GemvArgs a, int TP,
   }
 }
 
+// Prep kernel for the RMSNorm prologue: one 1024-thread CTA per token holds the
+// whole row in registers (item it = x[4it .. 4it+3]), so the row is read once:
+// sum of squares -> block reduction -> normalise -> digitise.
+constexpr int kNormPrepThreads = 1024;
+constexpr int kNormPrepMaxR = 8;  // items per thread: K <= 32768
+template <int IPU>
+__global__ void __launch_bounds__(kNormPrepThreads) act_prep_norm_kernel(const GemvArgs a, int TP,
+                                                                         int UPS) {
+  __shared__ float red[kNormPrepThreads / 32];
+  __shared__ float inv_s;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int tk = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nitems = a.KS * 64;
+  const int R = (nitems + kNormPrepThreads - 1) / kNormPrepThreads;
+  uint32_t* dig = (uint32_t*)a.dig;
+  float2* xsp = (float2*)(a.dig + (size_t)a.KS * 8 * TP * 128);
+  if (tk >= a.M) {  // padding token: zero digits and unit parameters
+    for (int r = 0; r < R; ++r) {
+      const int it = r * kNormPrepThreads + threadIdx.x;
+      if (it >= nitems) continue;
+      store_digits(dig, it >> 3, tk, TP, it & 7, Digits{{0u, 0u, 0u, 0u}, 0.f, 0.f});
+      if ((it % IPU) == 0) xsp[(it / IPU) * TP + tk] = make_float2(0.f, 0.f);
+    }
+    return;
+  }
+  float v[kNormPrepMaxR][4];
+  float ss = 0.f;
+#pragma unroll
+  for (int r = 0; r < kNormPrepMaxR; ++r) {
+    v[r][0] = v[r][1] = v[r][2] = v[r][3] = 0.f;
+    const int it = r * kNormPrepThreads + threadIdx.x;
+    if (r < R && it < nitems) {
+      load_raw4(a, tk * a.ldx + 4 * (int64_t)it, 4 * (int64_t)it, v[r]);
+      ss += v[r][0] * v[r][0] + v[r][1] * v[r][1] + v[r][2] * v[r][2] + v[r][3] * v[r][3];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  if (warp == 0) {
+    ss = red[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) inv_s = rsqrtf(ss / (float)a.n + a.eps);
+  }
+  __syncthreads();
+  const float inv = inv_s;
+  const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
+#pragma unroll
+  for (int r = 0; r < kNormPrepMaxR; ++r) {
+    if (r >= R) break;  // CTA-uniform
+    const int it = r * kNormPrepThreads + threadIdx.x;
+    const int64_t k = 4 * (int64_t)it;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[r][i] = (k + i < a.n) ? v[r][i] * inv * __ldg(a.xw + k + i) : 0.f;
+    const Digits d = digitize<IPU>(v[r], umask);
+    if (it < nitems) {
+      store_digits(dig, it >> 3, tk, TP, it & 7, d);
+      if ((it % IPU) == 0) xsp[(it / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
+    }
+  }
+}
+
 // Shared-memory carve-up (bytes), identical on host and device.
 struct SmemLayout {
   int ring, bars, bfrag, xs, zero, rbar, pbar, inv, yp, total, stage;
@@ -517,6 +583,7 @@ static int g_ring_kb = 0;     // tuning: ring bytes per CTA (KB; 0 = 10 KB per w
 static int g_max_ctas = 0;    // tuning: cap on the grid (0 = rule below)
 static int g_max_split = kMaxSplits;  // tuning: cap on the automatic K split (cluster size)
 static int g_carveout = -1;           // tuning: preferred shared-memory carveout (-1: default)
+static int g_norm_prep = 1;           // RMSNorm prologues via act_prep_norm_kernel (measured: -1 us per 7B layer)
 
 static int sm_count() {
   static int cached = 0;
@@ -642,7 +709,11 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   // block, else once per GEMV in act_prep_kernel
   const int rounds = (a.M * a.max_steps * 8 + WPC * 32 - 1) / (WPC * 32);
   a.dig = nullptr;
-  if (rounds > 2 || g_force_prep) {
+  // RMSNorm prologue for 1-2 tokens: one prep CTA per token (measured faster
+  // than every CTA re-reading the row on the 7B chain; slower at 8 tokens)
+  const bool norm_prep = a.xmode == 1 && a.M <= 2 && a.KS * 64 <= kNormPrepThreads * kNormPrepMaxR &&
+                         (rounds > 2 || g_force_prep || g_norm_prep);
+  if (rounds > 2 || g_force_prep || norm_prep) {
     const size_t bytes = (size_t)a.KS * 8 * TP * 128 + (size_t)a.KS * UPS * TP * 8;
     if (a.ws && a.ws_bytes >= bytes) {
       a.dig = a.ws;
@@ -659,7 +730,13 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     pa.val.programmaticStreamSerializationAllowed = 1;
     pc.attrs = &pa;
     pc.numAttrs = 1;
-    QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_kernel<IPU>, a, (int)TP, (int)UPS));
+    if (norm_prep) {
+      pc.gridDim = dim3(1, (unsigned)TP, 1);
+      pc.blockDim = dim3(kNormPrepThreads, 1, 1);
+      QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_norm_kernel<IPU>, a, (int)TP, (int)UPS));
+    } else {
+      QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_kernel<IPU>, a, (int)TP, (int)UPS));
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cols, (unsigned)S, 1);
@@ -719,6 +796,11 @@ extern "C" int qigen_debug_trace(void* buf) {
 
 extern "C" int qigen_debug_prefetch(int stages_before_wait) {
   g_pre = stages_before_wait;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_debug_norm_prep(int on) {
+  g_norm_prep = on;
   return QIGEN_OK;
 }
 

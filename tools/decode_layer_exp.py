@@ -62,6 +62,11 @@ def early():
     full(pf=False)
     Lb.qigen_debug_early_trigger(0)
 variants.append(("early trigger", early))
+def normprep():
+    Lb.qigen_debug_norm_prep(1)
+    full(pf=False)
+    Lb.qigen_debug_norm_prep(0)
+variants.append(("norm prep always", normprep))
 for ms in [1, 2, 3, 4, 8]:
     def f(ms=ms):
         Lb.qigen_debug_max_split(ms)
