@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(1024) rmsnorm_f16_kernel(const float* __restri
 // into the rank-0 CTA's shared memory (DSMEM); after one cluster barrier rank 0
 // combines the partials in split order (deterministic, no global round trip).
 constexpr int kAttnMaxSplit = 16;
+constexpr int kAttnThreads = 256;  // 8 warps (measured best: 128 and 512 slower, tools/attn_exp.py)
 
 struct AttnArgs {
   const float* qkv;  // [B, 3, H, HD] f32 (the fused QKV GEMV output)
@@ -113,7 +114,7 @@ __device__ __forceinline__ void attn_trace(const AttnArgs& a, int i) {
 // dynamic shared memory: K chunk | V chunk (f16 [chunk][HD] each) | scores
 // [chunk] | inbox [kAttnMaxSplit][HD + 2] (rank 0: every split's acc, m, l)
 template <int HD>
-__global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   __half* ks = (__half*)sm;
   __half* vs = ks + a.chunk * HD;
@@ -232,8 +233,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   // P V: thread = (dim pair, position residue class); half2 loads of V, the
   // NPH classes summed in fixed order; the partial state goes into the rank-0
   // CTA's inbox (distributed shared memory)
-  constexpr int NPAIR = HD / 2, NPH = 128 / NPAIR;  // 64 pairs x 2 or 32 x 4
-  __shared__ float2 pv[128];
+  constexpr int NPAIR = HD / 2, NPH = kAttnThreads / NPAIR;  // dim pairs x residue classes
+  __shared__ float2 pv[kAttnThreads];
   {
     const int dp = tid % NPAIR, ph = tid / NPAIR;
     float2 acc = make_float2(0.f, 0.f);
@@ -357,7 +358,7 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)a.nsplit, (unsigned)(batch * heads), 1);
-  cfg.blockDim = dim3(128, 1, 1);
+  cfg.blockDim = dim3(kAttnThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attrs[2];
