@@ -366,7 +366,8 @@ def run_decode(args):
     ctx = args.ctx or (512 if args.workload == "llama7b" else 1024)
     B = args.batch
     t0 = time.perf_counter()
-    model = D.LlamaTP(cfg, batch=B, max_ctx=ctx + 1, seed=0, tp=D.TP())
+    tp = D.ShardTP(args.tp_shard) if args.tp_shard > 1 else D.TP()
+    model = D.LlamaTP(cfg, batch=B, max_ctx=ctx + 1, seed=0, tp=tp)
     setup_s = time.perf_counter() - t0
     tok = torch.zeros(B, dtype=torch.long, device="cuda")
     pos = ctx  # ctx past tokens in the cache, this step writes position ctx
@@ -434,7 +435,10 @@ def run_decode(args):
             "data": "synthetic (random-init weights, random fp16 KV cache)",
             "config": {"workload": f"{args.workload} decode step", "layers": cfg.n_layers,
                        "d_model": cfg.d_model, "bits": cfg.bits, "group": cfg.group,
-                       "batch": B, "ctx": ctx, "parallelism": f"tp{world}",
+                       "batch": B, "ctx": ctx,
+                       "parallelism": (f"tp{args.tp_shard} shard of rank 0 on one GPU, collectives "
+                                       f"skipped (per-GPU compute only)") if args.tp_shard > 1
+                       else f"tp{world}",
                        "setup_s": round(setup_s, 1)},
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(gbs / peak, 4),
@@ -473,6 +477,9 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--ctx", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (smoke runs)")
+    ap.add_argument("--tp-shard", type=int, default=0,
+                    help="decode: time rank 0's shard of a TP group of this size on one GPU "
+                         "(collectives skipped: per-GPU compute only)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -129,6 +129,23 @@ class TP:
         return torch.cat([o[..., :s] for o, s in zip(outs, sizes)], dim=-1)
 
 
+class ShardTP(TP):
+    """One rank's shard of a TP group of `world` ranks on a single GPU, with the
+    collectives as no-ops: measures the per-GPU compute of a TP step (what the
+    step costs before communication), e.g. to bound TP scaling on a one-GPU
+    box.  Not for producing outputs."""
+
+    def __init__(self, world: int, rank: int = 0):
+        self.dist, self.group = None, None
+        self.rank, self.world = rank, world
+
+    def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+        return t
+
+    def all_gather_cat(self, t: torch.Tensor, sizes: list[int]) -> torch.Tensor:
+        return F.pad(t, (0, sum(sizes) - t.shape[-1]))
+
+
 # ---------------------------------------------------------------------------
 # linear backends
 # ---------------------------------------------------------------------------
