@@ -30,12 +30,13 @@ int main() {
   cudaFuncSetAttribute(k<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const int N = 100;
-  for (int mode = 0; mode < 12; ++mode) {
-    const int pdl = mode & 1, early = (mode >> 1) & 1, cl = (mode >> 2);  // cl: 0 none, 1 = 2, 2 = 7
-    const int csz = cl == 0 ? 1 : cl == 1 ? 2 : 7;
+  for (int mode = 0; mode < 16; ++mode) {
+    const int pdl = mode & 1, early = (mode >> 1) & 1, cl = (mode >> 2);  // cl: 0 none, 1 = 2, 2 = 7, 3 = alternate 9 / 6
+    const int csz0 = cl == 0 ? 1 : cl == 1 ? 2 : cl == 2 ? 7 : 9;
     cudaGraph_t g;
     cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
     for (int i = 0; i < N; ++i) {
+      const int csz = (cl == 3 && (i & 1)) ? 6 : csz0;
       cudaLaunchConfig_t c = {};
       c.gridDim = dim3(32, csz == 1 ? 6 : csz, 1);
       c.blockDim = 256; c.stream = s;
@@ -68,7 +69,7 @@ int main() {
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    printf("pdl=%d early=%d cluster=%d: %.2f us per kernel\n", pdl, early, csz, ms * 1e3 / (10 * N));
+    printf("pdl=%d early=%d cluster=%d%s: %.2f us per kernel\n", pdl, early, csz0, cl == 3 ? "/6 alternating" : "", ms * 1e3 / (10 * N));
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
