@@ -583,6 +583,9 @@ static int g_ring_kb = 0;     // tuning: ring bytes per CTA (KB; 0 = 10 KB per w
 static int g_max_ctas = 0;    // tuning: cap on the grid (0 = rule below)
 static int g_max_split = kMaxSplits;  // tuning: cap on the automatic K split (cluster size)
 static int g_carveout = -1;           // tuning: preferred shared-memory carveout (-1: default)
+}  // namespace qigen
+extern "C" int qigen_attn_set_carveout(int pct);  // decode_ops.cu
+namespace qigen {
 static int g_norm_prep = 1;           // RMSNorm prologues via act_prep_norm_kernel (measured: -1 us per 7B layer)
 
 static int sm_count() {
@@ -730,6 +733,14 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     pa.val.programmaticStreamSerializationAllowed = 1;
     pc.attrs = &pa;
     pc.numAttrs = 1;
+    static int prep_carveout = -2;
+    if (prep_carveout != g_carveout) {  // tuning aid: same carveout as the GEMV
+      prep_carveout = g_carveout;
+      QIGEN_CUDA_RET(cudaFuncSetAttribute(act_prep_kernel<IPU>,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout));
+      QIGEN_CUDA_RET(cudaFuncSetAttribute(act_prep_norm_kernel<IPU>,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout));
+    }
     if (norm_prep) {
       pc.gridDim = dim3(1, (unsigned)TP, 1);
       pc.blockDim = dim3(kNormPrepThreads, 1, 1);
@@ -806,6 +817,7 @@ extern "C" int qigen_debug_norm_prep(int on) {
 
 extern "C" int qigen_debug_carveout(int pct) {
   g_carveout = pct;
+  qigen_attn_set_carveout(pct);
   return QIGEN_OK;
 }
 
