@@ -338,6 +338,7 @@ class _Batch:
 
 
 _BATCHES: dict = {}
+_MAX_BATCHES = 8
 
 
 def qgemv_batch(pms, xs):
@@ -351,9 +352,12 @@ def qgemv_batch(pms, xs):
         raise ConfigError("qgemv_batch needs one activation vector per matrix")
     dev = _dev.require_cuda()
     key = tuple(id(pm) for pm in pms)
-    b = _BATCHES.get(key)
+    b = _BATCHES.pop(key, None)
     if b is None or any(p is not q for p, q in zip(b.pms, pms)):
-        b = _BATCHES[key] = _Batch(pms, dev)
+        b = _Batch(pms, dev)
+    _BATCHES[key] = b  # most recently used last
+    while len(_BATCHES) > _MAX_BATCHES:  # bounded: plans pin their matrices and buffers
+        _BATCHES.pop(next(iter(_BATCHES)))
     host = all(_dev.is_host(x) for x in xs)
     for i, (pw, x) in enumerate(zip(b.pws, xs)):
         shp = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
