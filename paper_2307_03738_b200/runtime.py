@@ -347,7 +347,8 @@ def qgemv_batch(pms, xs):
     [n_i] activation vector (numpy / CPU tensor, or CUDA f32 tensor).  Host
     inputs are staged through one pinned buffer (one H2D and one D2H copy per
     call) and numpy results are returned; device inputs give CUDA tensors.
-    The grouped plan and staging buffers are cached per matrix list."""
+    The grouped plan and staging buffers are cached per matrix list (the 8 most
+    recently used lists)."""
     if len(pms) != len(xs) or not pms:
         raise ConfigError("qgemv_batch needs one activation vector per matrix")
     dev = _dev.require_cuda()
