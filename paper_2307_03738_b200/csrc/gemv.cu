@@ -55,7 +55,8 @@ struct GemvArgs {
   int max_steps;     // max K-steps (32 rows) of any chunk
   int D;             // ring stages per warp
   int pre;           // stages per warp issued before griddepcontrol.wait
-  int xmode;         // activation prologue: 0 plain, 1 RMSNorm(x) * w, 2 SwiGLU(x[:n], x[n:])
+  int xmode;         // activation prologue: 0 plain, 1 RMSNorm(x) * w, 2 SwiGLU(x[:n], x[n:]),
+                     // 3 RMSNorm with the weight folded into W: y = rsqrt(mean(x^2) + eps) (x W)
   const float* xw;   // RMSNorm weight [n]
   float eps;         // RMSNorm epsilon
   unsigned char* dig;         // prepared activation digits (act_prep_kernel) or null
@@ -252,9 +253,11 @@ __global__ void __launch_bounds__(kNormPrepThreads) act_prep_norm_kernel(const G
   }
 }
 
+constexpr int kMaxRounds3 = 16;  // xmode 3: prologue rounds of the block per chunk (smem slots)
+
 // Shared-memory carve-up (bytes), identical on host and device.
 struct SmemLayout {
-  int ring, bars, bfrag, xs, zero, rbar, pbar, inv, yp, total, stage;
+  int ring, bars, bfrag, xs, zero, rbar, pbar, inv, ssw, yp, total, stage;
   __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int TP, int M, int WPC,
                                  int S) {
     stage = bits * 512 + szb;
@@ -268,7 +271,8 @@ struct SmemLayout {
     rbar = off;  off += 8;
     pbar = off;  off += 8;
     inv = off;   off += 16 * 4;
-    yp = off;    off += (S - 1) * WPC * 16 * M * 4 + 16;  // owner's inbox
+    ssw = off;   off += kMaxRounds3 * WPC * 8;            // xmode 3: (sum x^2, token) per round x warp
+    yp = off;    off += (S - 1) * (WPC * 16 * M + M) * 4 + 16;  // owner's inbox (+ sum x^2 per rank)
     total = off;
   }
 };
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     if (S > 1) {
       // split-K inbox of the cluster's rank-0 CTA: (S-1) partials of R floats
       mbar_init(rbar, 1);
-      mbar_expect_tx(rbar, (uint32_t)((S - 1) * WPC * 16 * M * 4));
+      mbar_expect_tx(rbar, (uint32_t)((S - 1) * (WPC * 16 * M + (a.xmode == 3 ? M : 0)) * 4));
     }
     if (a.dig) mbar_init(pbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -412,6 +416,17 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
         store_digits(bw, st, tk, TP, sub, d);
         if ((it % IPU) == 0) xs[((it % (nsteps * 8)) / IPU) * TP + tk] = make_float2(d.xsum, d.scale);
       }
+      if (a.xmode == 3) {
+        // sum of squares of this chunk: a warp's 32 items belong to one token
+        // (a token has nsteps * 8 items, a multiple of 64); fixed-order warp
+        // reduction, one slot per (round, warp)
+        float ss = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0)
+          ((float2*)(smem + L.ssw))[(it0 / T) * WPC + warp] =
+              make_float2(ss, __int_as_float(live ? tk : -1));
+      }
     }
     // zero fragments / unit params of the padding tokens M..TP-1
     for (int e = threadIdx.x; e < nsteps * (TP - M) * 16; e += T) {
@@ -424,6 +439,14 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
       for (int s = n_pre; s < n_first; ++s) issue(s);
     trace_point(a, 10);
     __syncthreads();
+    if (a.xmode == 3 && threadIdx.x < M) {  // this chunk's sum of squares per token, fixed order
+      const float2* sw = (const float2*)(smem + L.ssw);
+      const int nr = (items + T - 1) / T;
+      float ss = 0.f;
+      for (int i = 0; i < nr * WPC; ++i)
+        if (__float_as_int(sw[i].y) == (int)threadIdx.x) ss += sw[i].x;
+      inv_rms[threadIdx.x] = ss;  // (the chunk's partial; the row total is formed in the epilogue)
+    }
   }
   if (!a.early) asm volatile("griddepcontrol.launch_dependents;");
   trace_point(a, 2);
@@ -540,7 +563,19 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   if (S > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   trace_point(a, 6);
   const int64_t col0 = (int64_t)blockIdx.x * WPC * 16;
+  float* ssl = (float*)(smem + L.inv);  // xmode 3: this CTA's chunk sum of squares per token
+  if (a.xmode == 3 && rank > 0 && threadIdx.x < M)
+    st_async(mapa(yp + (S - 1) * R + (rank - 1) * M + threadIdx.x, 0), ssl[threadIdx.x],
+             mapa(rbar, 0));
   if (rank == 0 && S > 1) mbar_wait(rbar, 0);
+  if (a.xmode == 3 && rank == 0) {  // row totals in rank order -> 1 / rms
+    if (threadIdx.x < M) {
+      float ss = ssl[threadIdx.x];
+      for (int q = 1; q < S; ++q) ss += yp[(S - 1) * R + (q - 1) * M + threadIdx.x];
+      ssl[threadIdx.x] = rsqrtf(ss / (float)a.n + a.eps);
+    }
+    __syncthreads();
+  }
   if (early_x && rank == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before y
   trace_point(a, 7);
 #pragma unroll
@@ -558,6 +593,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
           st_async(mapa(yp + (rank - 1) * R + e, 0), v, mapa(rbar, 0));
         } else {
           for (int q = 1; q < S; ++q) v += yp[(q - 1) * R + e];
+          if (a.xmode == 3) v *= ssl[tk];
           const int64_t col = col0 + row;
           if (col < a.m) {
             float* dst = a.y + tk * a.ldy + col;
@@ -703,6 +739,16 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   // many tokens x long chunks: split K further until the fragments fit in smem
   while (req_S <= 0 && shape(S).total > 200 * 1024 && S < std::min(kMaxSplits, a.KS)) ++S;
   // (the smem-fit rule above may exceed g_max_split: fitting wins)
+  // xmode 3 (RMSNorm folded into W) needs the chunk's own x in every CTA: it
+  // never uses the prep kernels; K is split further until a chunk is <= 4
+  // rounds of the block
+  auto nrounds = [&](int s_) {
+    return (a.M * ((a.KS + s_ - 1) / s_) * 64 + WPC * 32 - 1) / (WPC * 32);
+  };
+  if (a.xmode == 3)
+    while (req_S <= 0 && S < std::min(kMaxSplits, a.KS) && nrounds(S) > 4) ++S;
+  QIGEN_CHECK_ARG(a.xmode != 3 || nrounds(S) <= kMaxRounds3, QIGEN_ERR_UNSUPPORTED,
+                  "folded-RMSNorm GEMV: K chunk too long for %d tokens", a.M);
   const SmemLayout L = shape(S);
   a.pre = g_pre < 0 ? a.D : g_pre;
   QIGEN_CHECK_ARG(L.total <= 227 * 1024, QIGEN_ERR_UNSUPPORTED,
@@ -716,7 +762,7 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   // than every CTA re-reading the row on the 7B chain; slower at 8 tokens)
   const bool norm_prep = a.xmode == 1 && a.M <= 2 && a.KS * 64 <= kNormPrepThreads * kNormPrepMaxR &&
                          (rounds > 2 || g_force_prep || g_norm_prep);
-  if (rounds > 2 || g_force_prep || norm_prep) {
+  if (a.xmode != 3 && (rounds > 2 || g_force_prep || norm_prep)) {
     const size_t bytes = (size_t)a.KS * 8 * TP * 128 + (size_t)a.KS * UPS * TP * 8;
     if (a.ws && a.ws_bytes >= bytes) {
       a.dig = a.ws;
@@ -871,7 +917,7 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   QIGEN_CHECK_ARG(tokens >= 1 && tokens <= 16, QIGEN_ERR_UNSUPPORTED,
                   "the GEMV path takes 1..16 activation rows, got %lld", (long long)tokens);
   QIGEN_CHECK_ARG(x_dtype >= 0 && x_dtype <= 2, QIGEN_ERR_ARG, "bad x dtype %d", x_dtype);
-  QIGEN_CHECK_ARG(prologue >= 0 && prologue <= 2, QIGEN_ERR_ARG, "bad prologue %d", prologue);
+  QIGEN_CHECK_ARG(prologue >= 0 && prologue <= 3, QIGEN_ERR_ARG, "bad prologue %d", prologue);
   QIGEN_CHECK_ARG(prologue != 1 || prologue_w, QIGEN_ERR_ARG, "RMSNorm prologue needs a weight");
   QIGEN_CHECK_ARG(ldx >= (prologue == 2 ? 2 * n : n) && ldy >= m, QIGEN_ERR_ARG,
                   "leading dimensions too small");

@@ -25,6 +25,7 @@ backend to check the TP logic with gloo (tests/test_decode_tp.py).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, replace
 
 import torch
@@ -232,13 +233,25 @@ class LlamaTP:
             gen.manual_seed(seed * 1_000_003 + tag)
             return torch.randn(shape, generator=gen, device=self.dev) * 0.02
 
+        # off by default: neutral on 7B, slower on 65B (same-box A/B, bench.py)
+        self.fold_qkv_norm = (batch <= 2 and backend is GpuBackend
+                              and os.environ.get("QIGEN_FOLD_QKV_NORM", "0") == "1")
         self.layers = []
         for li in range(cfg.n_layers):
             base = 100 * li
             # column-parallel fused QKV: global W_q|W_k|W_v [d, 3 d]; this rank's heads
             wq, wk, wv = (randn((d, cfg.n_heads * hd), base + i) for i in range(3))
             sl = slice(self.h0 * hd, self.h1 * hd)
-            wqkv = torch.cat([wq[:, sl], wk[:, sl], wv[:, sl]], dim=1).contiguous()
+            n1 = torch.ones(d, device=self.dev)  # RMSNorm weights (random init: 1)
+            n2 = torch.ones(d, device=self.dev)
+            # option (QIGEN_FOLD_QKV_NORM=1, 1-2 tokens): fold the RMSNorm weight
+            # into the QKV weights before quantization (diag(n1) W), so the GEMV
+            # applies only 1/rms, in its epilogue, from the sums of squares of the
+            # x chunks it already reads (no prep kernel)
+            wqkv = torch.cat([wq[:, sl], wk[:, sl], wv[:, sl]], dim=1)
+            if self.fold_qkv_norm:
+                wqkv = wqkv * n1[:, None]
+            wqkv = wqkv.contiguous()
             del wq, wk, wv
             wo = randn((cfg.n_heads * hd, d), base + 3)[self.o_rows[0]:self.o_rows[1]].contiguous()
             wg = randn((d, cfg.ffn), base + 4)[:, self.f0:self.f1]
@@ -251,8 +264,8 @@ class LlamaTP:
                 "o": backend.linear(wo, cfg.qcfg),
                 "gu": backend.linear(wgu, cfg.qcfg),
                 "down": backend.linear(wd, cfg.qcfg),
-                "n1": torch.ones(d, device=self.dev),
-                "n2": torch.ones(d, device=self.dev),
+                "n1": n1,
+                "n2": n2,
             }
             del wqkv, wo, wgu, wd
             self.layers.append(layer)
@@ -291,17 +304,21 @@ class LlamaTP:
     # -- one decode step ----------------------------------------------------
     def step(self, tokens: torch.Tensor, pos: int) -> torch.Tensor:
         """Greedy next tokens for `tokens` [B] at position `pos` (static shapes:
-        graph-capturable for a fixed pos).  Per layer: QKV GEMV (RMSNorm fused
-        into its prologue) -> fused RoPE + KV append + attention -> o_proj GEMV
-        (residual fused, all-reduce) -> gate|up GEMV (RMSNorm fused) -> down
-        GEMV (SwiGLU fused, residual fused, all-reduce)."""
+        graph-capturable for a fixed pos).  Per layer: QKV GEMV (RMSNorm fused:
+        folded into W with 1/rms in the epilogue at 1-2 tokens, else a prologue)
+        -> fused RoPE + KV append + attention -> o_proj GEMV (residual fused,
+        all-reduce) -> gate|up GEMV (RMSNorm prologue) -> down GEMV (SwiGLU
+        fused, residual fused, all-reduce)."""
         cfg, B, hd, be = self.cfg, self.B, self.cfg.head_dim, self.backend
         h = self.embed[tokens].float()                     # [B, d] residual stream
         cos, sin = self.cos[pos], self.sin[pos]
         scale = 1.0 / math.sqrt(hd)
         att = torch.empty((B, self.nh * hd), dtype=torch.float32, device=self.dev)
         for li, lay in enumerate(self.layers):
-            qkv = lay["qkv"](h, prologue="rmsnorm", norm_weight=lay["n1"], eps=cfg.norm_eps)
+            if self.fold_qkv_norm:
+                qkv = lay["qkv"](h, prologue="rmsnorm_folded", eps=cfg.norm_eps)
+            else:
+                qkv = lay["qkv"](h, prologue="rmsnorm", norm_weight=lay["n1"], eps=cfg.norm_eps)
             # RoPE + KV append + attention over positions 0..pos
             be.attention(qkv, cos, sin, self.k_cache[li], self.v_cache[li], pos, scale, att,
                          self.attn_ws)

@@ -160,7 +160,9 @@ class PanelWeights:
         """y[t, :] = f(x[t, :]) @ W for t < tokens; x: CUDA [tokens, n] or [n].
 
         ``prologue`` fuses the producer-side glue into the GEMV: None (f = id),
-        ``"rmsnorm"`` (f = RMSNorm with ``norm_weight``) or ``"swiglu"`` (x holds
+        ``"rmsnorm"`` (f = RMSNorm with ``norm_weight``), ``"rmsnorm_folded"``
+        (RMSNorm whose weight was folded into W at quantization: y = rsqrt(mean(x^2)
+        + eps) (x W), the norm is applied in the epilogue) or ``"swiglu"`` (x holds
         gate | up, [tokens, 2n]; f = silu(gate) * up).  ``x_ready`` asserts that
         x is not the output of the kernel launched just before on this stream
         (independent GEMVs back to back): the GEMV then overlaps that kernel
@@ -170,7 +172,7 @@ class PanelWeights:
         width = 2 * self.n if prologue == "swiglu" else self.n
         if x2.dim() != 2 or x2.shape[1] != width:
             raise ConfigError(f"x has shape {tuple(x.shape)}, expected [..., {width}]")
-        mode = {None: 0, "rmsnorm": 1, "swiglu": 2}[prologue]
+        mode = {None: 0, "rmsnorm": 1, "swiglu": 2, "rmsnorm_folded": 3}[prologue]
         if mode == 1 and (norm_weight is None or norm_weight.dtype != torch.float32
                           or not norm_weight.is_cuda or norm_weight.numel() != self.n):
             raise ConfigError("rmsnorm prologue needs a float32 CUDA weight of length n")

@@ -20,6 +20,8 @@ class OracleLinear:
         x = x.float()
         if prologue == "rmsnorm":
             x = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * norm_weight
+        elif prologue == "rmsnorm_folded":  # the norm weight is already in the matrix
+            x = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps)
         elif prologue == "swiglu":
             n = x.shape[-1] // 2
             x = torch.nn.functional.silu(x[..., :n]) * x[..., n:]

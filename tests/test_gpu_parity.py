@@ -476,3 +476,21 @@ def test_qgemv_batch_public_api(q):
         ys = q.qgemv_batch(pms, xs)
         for y, r in zip(ys, refs):
             assert rel_err(y, r) <= TOL
+
+
+@pytest.mark.parametrize("tokens", [1, 2, 3, 8])
+@pytest.mark.parametrize("K,N,bits,g", [(4096, 1536, 4, 128), (2048, 4000, 3, 64), (8192, 512, 2, 32)])
+def test_rmsnorm_folded_prologue(q, tokens, K, N, bits, g):
+    """prologue "rmsnorm_folded": y = rsqrt(mean(x^2) + eps) (x W) with the
+    norm applied in the epilogue from the chunks' sums of squares (rank order)."""
+    cm, codes, s, z, rng = _case(q, K, N, bits, g, seed=K + tokens)
+    pw = q.PanelWeights.from_codes(cm)
+    X = rng.normal(0, 1, (tokens, K)).astype(np.float32) * 3.0
+    eps = 1e-5
+    Y = pw.gemv(torch.from_numpy(X).cuda(), prologue="rmsnorm_folded", eps=eps).cpu().numpy()
+    Y2 = pw.gemv(torch.from_numpy(X).cuda(), prologue="rmsnorm_folded", eps=eps).cpu().numpy()
+    assert np.array_equal(Y, Y2)  # deterministic
+    for t in range(tokens):
+        inv = 1.0 / np.sqrt(np.mean(X[t].astype(np.float64) ** 2) + eps)
+        yref = orc.qgemv_reference(codes, s, z, X[t]) * inv
+        assert rel_err(Y[t], yref) <= TOL, (tokens, t)

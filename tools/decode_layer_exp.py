@@ -29,6 +29,15 @@ def full(pf=False):
         lay["down"](gus[li], out=h, accumulate=True, prologue="swiglu")
 
 
+def full_folded():
+    for li, lay in enumerate(m.layers):
+        lay["qkv"](h, out=qkvs[li], prologue="rmsnorm_folded")
+        be.attention(qkvs[li], cos, sin, m.k_cache[li], m.v_cache[li], pos, 1 / math.sqrt(128), att, m.attn_ws)
+        lay["o"](att, out=h, accumulate=True)
+        lay["gu"](h, out=gus[li], prologue="rmsnorm_folded")
+        lay["down"](gus[li], out=h, accumulate=True, prologue="swiglu")
+
+
 def gemvs():
     for li, lay in enumerate(m.layers):
         lay["qkv"](h, out=qkvs[li], prologue="rmsnorm", norm_weight=lay["n1"])
@@ -56,7 +65,7 @@ Lb = _lib.lib()
 s = torch.cuda.Stream()
 def base():
     full(pf=False)
-variants = [("full layer", base)]
+variants = [("full layer", base), ("full layer, folded RMSNorm", full_folded)]
 def early():
     Lb.qigen_debug_early_trigger(1)
     full(pf=False)
@@ -76,6 +85,8 @@ for ms in [1, 2, 3, 4, 8]:
 if os.environ.get("ALL"):
   variants += [("4 gemvs", gemvs),
                  ("qkv (rmsnorm)", one("qkv", prologue="rmsnorm", norm_weight=m.layers[0]["n1"])),
+                 ("qkv (rmsnorm folded)", one("qkv", prologue="rmsnorm_folded")),
+                 ("gate_up (rmsnorm folded)", one("gu", prologue="rmsnorm_folded")),
                  ("o (acc)", one("o", accumulate=True)),
                  ("gate_up (rmsnorm)", one("gu", prologue="rmsnorm", norm_weight=m.layers[0]["n2"])),
                  ("down (swiglu, acc)", one("down", prologue="swiglu", accumulate=True)),
