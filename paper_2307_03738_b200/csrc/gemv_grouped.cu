@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <queue>
 #include <utility>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -445,54 +446,61 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
     const bool active = p < f.P;
     const int combo = f.combo;
     const int K0 = f.k0, K1 = f.k1;  // registers (see the producer)
-    const int wb = f.wb, zpj = (f.gps > 0 ? f.gps : 1) * 128;
     float* const yg = f.y;
     const int64_t ldy = f.ldy;
     const int M = f.M, m = f.m, split = f.split;
     float yv[2] = {0.f, 0.f};
-    for (int s = K0; s < K1; s += kGSS) {
-      const int nss = min(kGSS, K1 - s);
-      mbar_wait(&rfull[rslot], rph);
-      if (active) {
-        mbar_wait(&full[wslot], wph);
-        const unsigned char* stg = ring + wslot * kGSlot;
-        const unsigned char* rec = rring + rslot * kRecSlot;
-        if (pl.mode != 1) {
-          for (int j = 0; j < nss; ++j) {
-            const unsigned char* wj = stg + j * wb;
-            const float2* zj = (const float2*)(stg + kGSS * wb + j * zpj);
-            const unsigned char* rj = rec + j * kRecBytes;
-            switch (combo) {
-#define QG_CASE(B, G)                                                                         \
-  case (B - 2) * 5 + G: {                                                                     \
-    uint4 w[B];                                                                               \
-    _Pragma("unroll") for (int v = 0; v < B; ++v) w[v] = ((const uint4*)wj)[v * 32 + lane];  \
-    group_superstep<B, G>(w, zj, rj, yv);                                                     \
-  } break;
-              QG_CASE(2, 0) QG_CASE(2, 1) QG_CASE(2, 2) QG_CASE(2, 4) QG_CASE(2, 8)
-              QG_CASE(3, 0) QG_CASE(3, 1) QG_CASE(3, 2) QG_CASE(3, 4) QG_CASE(3, 8)
-              QG_CASE(4, 0) QG_CASE(4, 1) QG_CASE(4, 2) QG_CASE(4, 4) QG_CASE(4, 8)
-#undef QG_CASE
-              default: break;
+    // the item's stage loop, specialised per (bits, groups per superstep): no
+    // dispatch inside the loop, compile-time stage geometry
+    auto stage_loop = [&](auto bits_c, auto gps_c) {
+      constexpr int B = decltype(bits_c)::value, G = decltype(gps_c)::value;
+      constexpr int WB = B * 512, ZPJ = (G > 0 ? G : 1) * 128;
+      for (int s = K0; s < K1; s += kGSS) {
+        const int nss = min(kGSS, K1 - s);
+        mbar_wait(&rfull[rslot], rph);
+        if (active) {
+          mbar_wait(&full[wslot], wph);
+          const unsigned char* stg = ring + wslot * kGSlot;
+          const unsigned char* rec = rring + rslot * kRecSlot;
+          if (pl.mode != 1) {
+#pragma unroll
+            for (int j = 0; j < kGSS; ++j) {
+              if (j < nss) {
+                uint4 w[B];
+#pragma unroll
+                for (int v = 0; v < B; ++v) w[v] = ((const uint4*)(stg + j * WB))[v * 32 + lane];
+                group_superstep<B, G>(w, (const float2*)(stg + kGSS * WB + j * ZPJ),
+                                      rec + j * kRecBytes, yv);
+              }
             }
+          }
+          __syncwarp();
+          if (lane == 0 && !cdone) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_one(true);
+          }
+          if (++wslot == kGDepth) {
+            wslot = 0;
+            wph ^= 1u;
           }
         }
         __syncwarp();
-        if (lane == 0 && !cdone) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_one(true);
-        }
-        if (++wslot == kGDepth) {
-          wslot = 0;
-          wph ^= 1u;
+        if (lane == 0) mbar_arrive(&rempty[rslot]);
+        if (++rslot == kGRecDepth) {
+          rslot = 0;
+          rph ^= 1u;
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&rempty[rslot]);
-      if (++rslot == kGRecDepth) {
-        rslot = 0;
-        rph ^= 1u;
-      }
+    };
+    using std::integral_constant;
+    switch (combo) {
+#define QG_CASE(B, G) \
+  case (B - 2) * 5 + G: stage_loop(integral_constant<int, B>{}, integral_constant<int, G>{}); break;
+      QG_CASE(2, 0) QG_CASE(2, 1) QG_CASE(2, 2) QG_CASE(2, 4) QG_CASE(2, 8)
+      QG_CASE(3, 0) QG_CASE(3, 1) QG_CASE(3, 2) QG_CASE(3, 4) QG_CASE(3, 8)
+      QG_CASE(4, 0) QG_CASE(4, 1) QG_CASE(4, 2) QG_CASE(4, 4) QG_CASE(4, 8)
+#undef QG_CASE
+      default: break;
     }
     if (active) {
       const int gq = lane >> 2, t = lane & 3;
