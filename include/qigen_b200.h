@@ -121,7 +121,10 @@ int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int b
 /* qigen_gemv with a fused activation prologue (the decode driver's glue):
  *   prologue 0: x as given;
  *   prologue 1: RMSNorm, x_k * rsqrt(mean_k(x^2) + eps) * prologue_w[k] (LLaMA RMSNorm);
- *   prologue 2: SwiGLU, silu(x[t, k]) * x[t, n + k] (x holds gate | up, ldx >= 2n).
+ *   prologue 2: SwiGLU, silu(x[t, k]) * x[t, n + k] (x holds gate | up, ldx >= 2n);
+ *   prologue 3: RMSNorm with its weight folded into W at quantization: y[t] =
+ *     rsqrt(mean_k(x[t]^2) + eps) * (x[t] W), the 1/rms applied in the epilogue
+ *     from the sums of squares of the x chunks (fixed reduction order).
  * workspace (device, >= qigen_gemv_workspace_size bytes, or NULL): scratch for the
  * activation digits when they are prepared once per call (long K chunks / many
  * tokens); NULL uses a grow-only library buffer that cannot grow during capture. */
