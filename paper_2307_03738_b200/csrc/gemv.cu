@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   // (with x_ready the inputs are known not to come from the preceding kernel:
   // only the y write below waits, so this GEMV overlaps its predecessor fully)
   const bool early_x = a.x_ready && !a.dig;
+  trace_point(a, 9);
   if (!early_x) asm volatile("griddepcontrol.wait;" ::: "memory");
   trace_point(a, 1);
 

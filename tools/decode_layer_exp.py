@@ -76,7 +76,13 @@ def normprep():
     full(pf=False)
     Lb.qigen_debug_norm_prep(0)
 variants.append(("norm prep always", normprep))
-for ms in [1, 2, 3, 4, 8]:
+for pre in [0, 1, 2]:
+    def fp(pre=pre):
+        Lb.qigen_debug_prefetch(pre)
+        full(pf=False)
+        Lb.qigen_debug_prefetch(-1)
+    variants.append((f"pre-wait stages {pre}", fp))
+for ms in []:
     def f(ms=ms):
         Lb.qigen_debug_max_split(ms)
         full(pf=False)

@@ -72,6 +72,11 @@ for key in sorted(bufs, key=lambda k: int(bufs[k].view(-1, 16)[:, 0][bufs[k].vie
     print(f"{str(key):14s} n={len(t):4d} entry {r[:,0].min():7.2f}-{r[:,0].max():7.2f} wait {r[:,1].min():7.2f}-{r[:,1].max():7.2f} "
           f"prol {np.median(r[:,2]):7.2f} loop {np.median(r[:,3]):7.2f}/{r[:,3].max():7.2f} exit {r[:,4].min():7.2f}-{r[:,4].max():7.2f}")
 
+print("entry -> before wait -> after wait (SM cycles, median):")
+for key in [(3, "qkv"), (3, "o"), (3, "gu"), (3, "down")]:
+    t = cbufs[key].view(-1, 16).cpu().numpy()
+    t = t[t[:, 0] > 0].astype(np.int64)
+    print(key, f"setup {np.median(t[:, 9] - t[:, 0]):.0f}  wait {np.median(t[:, 1] - t[:, 9]):.0f}")
 print("phases in SM cycles after the PDL wait (median): xload dig1 digits sync stage0 loop exit")
 for key in [(3, "qkv"), (3, "o"), (3, "gu"), (3, "down")]:
     t = cbufs[key].view(-1, 16).cpu().numpy()
