@@ -337,6 +337,26 @@ class _Batch:
         self.group = GemvGroup([(pw, self.x[self.koff[i]:self.koff[i + 1]],
                                  self.y[self.noff[i]:self.noff[i + 1]])
                                 for i, pw in enumerate(self.pws)])
+        self.graph = None  # host path: H2D -> grouped launch -> D2H as one graph
+
+    def host_round_trip(self) -> None:
+        """xh -> x, the grouped GEMVs, y -> yh, replayed as one CUDA graph
+        (captured on first use) on a private stream; blocks until done."""
+        if self.graph is None:
+            self.stream = torch.cuda.Stream()
+            with torch.cuda.stream(self.stream):
+                self.x.copy_(self.xh, non_blocking=True)
+                self.group.run()
+                self.stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self.x.copy_(self.xh, non_blocking=True)
+                    self.group.run()
+                    self.yh.copy_(self.y, non_blocking=True)
+            self.graph = g
+        self.stream.wait_stream(torch.cuda.current_stream())
+        self.graph.replay()
+        self.stream.synchronize()
 
 
 _BATCHES: dict = {}
@@ -367,17 +387,14 @@ def qgemv_batch(pms, xs):
         if shp != (pw.n,):
             raise ConfigError(f"x[{i}] has shape {shp}, expected [{pw.n}]")
     if host:
-        # one host-side gather into the pinned staging buffer, one H2D copy
+        # one host-side gather into the pinned staging buffer, then one graph:
+        # H2D copy, grouped launch, D2H copy
         np.concatenate([x.numpy() if isinstance(x, torch.Tensor) else x for x in xs],
                        out=b.xh_np, casting="same_kind")
-        b.x.copy_(b.xh, non_blocking=True)
-    else:
-        torch.cat([x.reshape(-1).float() for x in xs], out=b.x)
-    b.group.run()
-    if host:
-        b.yh.copy_(b.y, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        b.host_round_trip()
         return np.split(b.yh_np.copy(), b.noff[1:-1])
+    torch.cat([x.reshape(-1).float() for x in xs], out=b.x)
+    b.group.run()
     return list(torch.split(b.y.clone(), [pw.m for pw in b.pws]))
 
 
