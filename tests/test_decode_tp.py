@@ -132,3 +132,18 @@ def test_fused_attention_vs_sdpa(B, H, ctx, pos):
     OracleBackend.attention(qkv, cos, sin, kc2, vc2, pos, 1 / math.sqrt(hd), ref, None)
     assert ((out - ref).abs().max() / (1 + ref.abs().max())).item() < 1e-5
     assert torch.equal(kc, kc2) and torch.equal(vc, vc2)
+
+
+def test_shard_tp_is_a_compute_only_stand_in():
+    """ShardTP: rank 0 of a `world`-rank group on one device, collectives as
+    no-ops with the full logit width restored (bench.py --tp-shard)."""
+    tp = D.ShardTP(4)
+    assert (tp.rank, tp.world) == (0, 4)
+    t = torch.ones(2, 5)
+    assert tp.all_reduce(t) is t
+    assert tuple(tp.all_gather_cat(t, [5, 5, 4, 4]).shape) == (2, 18)
+    m = D.LlamaTP(TINY, batch=1, max_ctx=8, seed=1, device="cpu", tp=tp,
+                  backend=__import__("decode_backends").OracleBackend, kv_dtype=torch.float32)
+    assert m.nh == TINY.n_heads // 4
+    out = m.step(torch.tensor([3]), pos=2)
+    assert tuple(out.shape) == (1,)

@@ -494,3 +494,17 @@ def test_rmsnorm_folded_prologue(q, tokens, K, N, bits, g):
         inv = 1.0 / np.sqrt(np.mean(X[t].astype(np.float64) ** 2) + eps)
         yref = orc.qgemv_reference(codes, s, z, X[t]) * inv
         assert rel_err(Y[t], yref) <= TOL, (tokens, t)
+
+
+def test_qgemv_batch_device_inputs(q):
+    """qgemv_batch with CUDA tensors in and out (no host staging)."""
+    pms, xs, refs = [], [], []
+    for i, (K, N, b, g) in enumerate([(512, 256, 4, 64), (768, 100, 3, None)]):
+        cm, codes, s, z, rng = _case(q, K, N, b, g, seed=60 + i)
+        pms.append(q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N))))
+        x = rng.normal(0, 1, K).astype(np.float32)
+        xs.append(torch.from_numpy(x).cuda())
+        refs.append(orc.qgemv_reference(codes, s, z, x))
+    ys = q.qgemv_batch(pms, xs)
+    for y, r in zip(ys, refs):
+        assert y.is_cuda and rel_err(y.cpu().numpy(), r) <= TOL
