@@ -18,6 +18,7 @@ and errors, backed by libqigen_b200:
 from __future__ import annotations
 
 from dataclasses import dataclass
+import os
 
 import numpy as np
 import torch
@@ -354,13 +355,15 @@ class _Batch:
                     self.group.run()
                     self.yh.copy_(self.y, non_blocking=True)
             self.graph = g
-        self.stream.wait_stream(torch.cuda.current_stream())
-        self.graph.replay()
+        self.stream.wait_stream(torch.cuda.current_stream())  # e.g. the re-tiling
+        with torch.cuda.stream(self.stream):  # replay() launches on the current stream
+            self.graph.replay()
         self.stream.synchronize()
 
 
 _BATCHES: dict = {}
 _MAX_BATCHES = 8
+_BATCH_GRAPH = [os.environ.get("QIGEN_BATCH_GRAPH", "0") == "1"]  # host path as one CUDA graph (A/B: slower)
 
 
 def qgemv_batch(pms, xs):
@@ -391,7 +394,13 @@ def qgemv_batch(pms, xs):
         # H2D copy, grouped launch, D2H copy
         np.concatenate([x.numpy() if isinstance(x, torch.Tensor) else x for x in xs],
                        out=b.xh_np, casting="same_kind")
-        b.host_round_trip()
+        if _BATCH_GRAPH[0]:
+            b.host_round_trip()
+        else:
+            b.x.copy_(b.xh, non_blocking=True)
+            b.group.run()
+            b.yh.copy_(b.y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
         return np.split(b.yh_np.copy(), b.noff[1:-1])
     torch.cat([x.reshape(-1).float() for x in xs], out=b.x)
     b.group.run()
