@@ -738,7 +738,7 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   if (req_S <= 0) S = std::min(S, g_max_split);
   QIGEN_CHECK_ARG(S >= 1 && S <= a.KS && S <= kMaxSplits, QIGEN_ERR_ARG, "k_splits %d out of range", S);
   // many tokens x long chunks: split K further until the fragments fit in smem
-  while (req_S <= 0 && shape(S).total > 200 * 1024 && S < std::min(kMaxSplits, a.KS)) ++S;
+  while (req_S <= 0 && shape(S).total > 224 * 1024 && S < std::min(kMaxSplits, a.KS)) ++S;
   // (the smem-fit rule above may exceed g_max_split: fitting wins)
   // xmode 3 (RMSNorm folded into W) needs the chunk's own x in every CTA: it
   // never uses the prep kernels; K is split further until a chunk is <= 4
