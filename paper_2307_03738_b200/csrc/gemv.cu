@@ -691,6 +691,13 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   const int cols = (a.P + WPC - 1) / WPC;
   int S = req_S;
   const int sms = sm_count();
+  if (S <= 0 && a.M >= 4) {
+    // 4+ tokens: the loop is issue-bound (NB n8 blocks per step), so fewer,
+    // longer chunks win; 2 splits unless the fragments need more shared memory
+    // (measured on the 65B B=8 shapes: 8192x24576 63 vs 75 us, 8192x44032 103 vs
+    // 122 us; tools/microbench.py --tokens 8 --splits ...)
+    S = std::min(2, a.KS);
+  }
   if (S <= 0 && (int64_t)cols * a.KS >= (int64_t)sms * 24) {
     // Large matrices are streaming-bound: pick the split whose grid fills whole
     // waves of SMs best (an SM holding one CTA more than its neighbours sets the

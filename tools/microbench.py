@@ -38,7 +38,11 @@ for shp in args.shapes.split(","):
                     def run():
                         for pw in pws:
                             pw.gemv(x, out=y, k_splits=ks)
-                    run(); torch.cuda.synchronize()
+                    try:
+                        run(); torch.cuda.synchronize()
+                    except Exception as e:  # noqa: BLE001 (split does not fit)
+                        print(json.dumps(dict(K=K, N=N, bits=b, g=gs, tokens=T, splits=ks, err=str(e)[:50])))
+                        continue
                     if args.graph:
                         gph = torch.cuda.CUDAGraph()
                         with torch.cuda.graph(gph):
