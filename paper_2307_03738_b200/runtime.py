@@ -18,7 +18,6 @@ and errors, backed by libqigen_b200:
 from __future__ import annotations
 
 from dataclasses import dataclass
-import os
 
 import numpy as np
 import torch
@@ -333,37 +332,14 @@ class _Batch:
         self.x = torch.zeros(int(self.koff[-1]), device=dev)
         self.y = torch.zeros(int(self.noff[-1]), device=dev)
         self.xh = torch.zeros(int(self.koff[-1])).pin_memory()
-        self.yh = torch.zeros(int(self.noff[-1])).pin_memory()
-        self.xh_np, self.yh_np = self.xh.numpy(), self.yh.numpy()
+        self.xh_np = self.xh.numpy()
         self.group = GemvGroup([(pw, self.x[self.koff[i]:self.koff[i + 1]],
                                  self.y[self.noff[i]:self.noff[i + 1]])
                                 for i, pw in enumerate(self.pws)])
-        self.graph = None  # host path: H2D -> grouped launch -> D2H as one graph
-
-    def host_round_trip(self) -> None:
-        """xh -> x, the grouped GEMVs, y -> yh, replayed as one CUDA graph
-        (captured on first use) on a private stream; blocks until done."""
-        if self.graph is None:
-            self.stream = torch.cuda.Stream()
-            with torch.cuda.stream(self.stream):
-                self.x.copy_(self.xh, non_blocking=True)
-                self.group.run()
-                self.stream.synchronize()
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=self.stream):
-                    self.x.copy_(self.xh, non_blocking=True)
-                    self.group.run()
-                    self.yh.copy_(self.y, non_blocking=True)
-            self.graph = g
-        self.stream.wait_stream(torch.cuda.current_stream())  # e.g. the re-tiling
-        with torch.cuda.stream(self.stream):  # replay() launches on the current stream
-            self.graph.replay()
-        self.stream.synchronize()
 
 
 _BATCHES: dict = {}
 _MAX_BATCHES = 8
-_BATCH_GRAPH = [os.environ.get("QIGEN_BATCH_GRAPH", "0") == "1"]  # host path as one CUDA graph (A/B: slower)
 
 
 def qgemv_batch(pms, xs):
@@ -371,37 +347,46 @@ def qgemv_batch(pms, xs):
     matrices, as ONE grouped GPU launch (``GemvGroup``).  ``xs``: per matrix an
     [n_i] activation vector (numpy / CPU tensor, or CUDA f32 tensor).  Host
     inputs are staged through one pinned buffer (one H2D and one D2H copy per
-    call) and numpy results are returned; device inputs give CUDA tensors.
+    call) and numpy results are returned (views of one fresh pinned block);
+    device inputs give CUDA tensors.
     The grouped plan and staging buffers are cached per matrix list (the 8 most
     recently used lists)."""
     if len(pms) != len(xs) or not pms:
         raise ConfigError("qgemv_batch needs one activation vector per matrix")
-    dev = _dev.require_cuda()
-    key = tuple(id(pm) for pm in pms)
+    key = tuple(map(id, pms))
     b = _BATCHES.pop(key, None)
     if b is None or any(p is not q for p, q in zip(b.pms, pms)):
-        b = _Batch(pms, dev)
+        b = _Batch(pms, _dev.require_cuda())  # fails loudly without a GPU
     _BATCHES[key] = b  # most recently used last
     while len(_BATCHES) > _MAX_BATCHES:  # bounded: plans pin their matrices and buffers
         _BATCHES.pop(next(iter(_BATCHES)))
-    host = all(_dev.is_host(x) for x in xs)
+    host = True
+    hx = []  # host arrays for the gather
     for i, (pw, x) in enumerate(zip(b.pws, xs)):
-        shp = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
-        if shp != (pw.n,):
-            raise ConfigError(f"x[{i}] has shape {shp}, expected [{pw.n}]")
+        if type(x) is not np.ndarray:
+            if isinstance(x, torch.Tensor):
+                if x.is_cuda:
+                    host = False
+                else:
+                    x = x.numpy()
+            else:
+                x = np.asarray(x)
+        if x.shape != (pw.n,):
+            raise ConfigError(f"x[{i}] has shape {tuple(x.shape)}, expected [{pw.n}]")
+        hx.append(x)
     if host:
-        # one host-side gather into the pinned staging buffer, then one graph:
-        # H2D copy, grouped launch, D2H copy
-        np.concatenate([x.numpy() if isinstance(x, torch.Tensor) else x for x in xs],
-                       out=b.xh_np, casting="same_kind")
-        if _BATCH_GRAPH[0]:
-            b.host_round_trip()
-        else:
-            b.x.copy_(b.xh, non_blocking=True)
-            b.group.run()
-            b.yh.copy_(b.y, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-        return np.split(b.yh_np.copy(), b.noff[1:-1])
+        # one host-side gather into the pinned staging buffer, one H2D copy,
+        # the grouped launch, one D2H copy
+        np.concatenate(hx, out=b.xh_np, casting="same_kind")
+        b.x.copy_(b.xh, non_blocking=True)
+        b.group.run()
+        # results land in a fresh pinned block (torch's caching host allocator:
+        # no cudaHostAlloc after warm-up) that the returned views own, so no
+        # host-side copy out of a shared staging buffer is needed
+        yh = torch.empty(b.y.numel(), pin_memory=True)
+        yh.copy_(b.y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return np.split(yh.numpy(), b.noff[1:-1])
     torch.cat([x.reshape(-1).float() for x in xs], out=b.x)
     b.group.run()
     return list(torch.split(b.y.clone(), [pw.m for pw in b.pws]))
