@@ -18,6 +18,8 @@ ap.add_argument("--splits", default="0")
 ap.add_argument("--tokens", default="1")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--graph", action="store_true")
+ap.add_argument("--group", action="store_true", help="the R copies as one GemvGroup launch (tokens <= 2)")
+ap.add_argument("--x-ready", action="store_true", help="independent GEMVs (QIGEN_GEMV_X_READY)")
 args = ap.parse_args()
 dev = torch.device("cuda")
 res = []
@@ -35,9 +37,14 @@ for shp in args.shapes.split(","):
                 x = torch.randn(T, K, device=dev)
                 y = torch.empty(T, N, device=dev)
                 for ks in map(int, args.splits.split(",")):
-                    def run():
-                        for pw in pws:
-                            pw.gemv(x, out=y, k_splits=ks)
+                    if args.group:
+                        ys = torch.empty(R, T, N, device=dev)
+                        grp = q.GemvGroup([(pw, x, ys[i]) for i, pw in enumerate(pws)])
+                        run = grp.run
+                    else:
+                        def run():
+                            for pw in pws:
+                                pw.gemv(x, out=y, k_splits=ks, x_ready=args.x_ready)
                     try:
                         run(); torch.cuda.synchronize()
                     except Exception as e:  # noqa: BLE001 (split does not fit)
