@@ -22,7 +22,8 @@
 //     to the model's errors; the claimer stages the item's geometry in shared
 //     memory, normally a few stages before it is needed;
 //   * each consumer warp streams its panel of every item through its own ring
-//     of TMA bulk-copy stages (2 supersteps of weights + their (s, z)), refilled
+//     of TMA bulk-copy stages (2 supersteps of weights + their (s, z); 4 for
+//     2-bit weights, whose per-stage issue cost would otherwise dominate), refilled
 //     by its lane 0 ahead ACROSS item boundaries, so the weight stream never
 //     drains between GEMVs and a slow copy stalls only its own panel;
 //   * the producer warp streams the activation records through a CTA-shared
@@ -49,8 +50,14 @@ constexpr int kRecDig = 8 * kGTP * 128;  // digit bytes per superstep record
 // + per unit and token {2^(E-30) * 2^16, X * 2^(E-30), 2^(E-30), 0}: the flush
 // factors of the even (digits d0 d1) and odd (d2 d3) lanes, one LDS.64 each
 constexpr int kRecBytes = kRecDig + 8 * kGTP * 16;
-constexpr int kGSS = 2;                // supersteps per ring stage
+constexpr int kGSS = 2;                // supersteps per activation-record stage
 constexpr int kGSlot = kGSS * (4 * 512 + 8 * 128);  // largest weight stage (4-bit, g = 32)
+// Supersteps per WEIGHT stage: 4 where they fit a slot (2-bit weights with at
+// most 4 groups per superstep), else kGSS.  Each stage costs the issuing lane
+// a fixed overhead while its warp waits, so small-bit stages are made longer.
+__host__ __device__ constexpr int wss_for(int bits, int gps) {
+  return bits == 2 && gps <= 4 ? 2 * kGSS : kGSS;
+}
 constexpr int kGDepth = 2;             // weight stages per consumer warp
 constexpr int kRecSlot = kGSS * kRecBytes;
 constexpr int kGRecDepth = 4;          // activation-record stages in the CTA ring
@@ -316,13 +323,13 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
   // ---- weight prefetch of item 0 (independent of every other kernel) --------
   unsigned char* ring = smem + warp * kGDepth * kGSlot;
   uint64_t* full = wfull + warp * kGDepth;
-  // Issue cursor (lane 0) over this warp's stream of stages (kGSS supersteps of
-  // its panel: weights, then the (s, z) of their groups at offset kGSS * wb),
+  // Issue cursor (lane 0) over this warp's stream of stages (wss_for supersteps
+  // of its panel: weights, then the (s, z) of their groups at offset wss * wb),
   // skipping items in which the warp has no panel (ragged last item of a
   // GEMV); the current item's geometry is cached in registers.
   int ck = 0, cs = 0, islot = 0;  // cursor: sequence index, superstep, ring slot
   bool cdone = false;
-  int c_k1 = 0, c_gps = 0, c_g = 0;
+  int c_k1 = 0, c_gps = 0, c_g = 0, c_wss = kGSS;
   uint32_t c_wb = 0;
   const char *c_w = nullptr, *c_z = nullptr;
   auto load_item = [&]() {
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
         c_gps = f.gps;
         c_g = f.g;
         c_wb = f.wb;
+        c_wss = wss_for(f.wb / 512, f.gps);
         c_w = f.w + warp * f.wstride;
         c_z = f.z + warp * f.zstride;
         return;
@@ -348,18 +356,20 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
   // when `advance` is off (the first ring fill stays inside item 0: claiming a
   // later item waits for the prep kernel)
   auto issue_one = [&](bool advance) {
-    const int nss = min(kGSS, c_k1 - cs);
+    const int nss = min(c_wss, c_k1 - cs);
     unsigned char* dst = ring + islot * kGSlot;
     uint64_t* bar = &full[islot];
-    const uint32_t zb = (uint32_t)((c_gps > 0 ? nss * c_gps : nss) * 128);
+    const uint32_t zb = (uint32_t)((c_gps > 0 ? nss * c_gps : c_g ? nss : 1) * 128);
     mbar_expect_tx(bar, nss * c_wb + zb);
     bulk_g2s(dst, c_w + (int64_t)cs * c_wb, nss * c_wb, bar);
     if (c_gps > 0) {
-      bulk_g2s(dst + kGSS * c_wb, c_z + (int64_t)cs * c_gps * 128, zb, bar);
+      bulk_g2s(dst + c_wss * c_wb, c_z + (int64_t)cs * c_gps * 128, zb, bar);
+    } else if (c_g == 0) {  // full column: one group for the whole stage
+      bulk_g2s(dst + c_wss * c_wb, c_z, 128, bar);
     } else {  // one group per superstep: the one containing it
       for (int j = 0; j < nss; ++j) {
         const int64_t gi = c_g ? (int64_t)(cs + j) * kSuper / c_g : 0;
-        bulk_g2s(dst + kGSS * c_wb + j * 128, c_z + gi * 128, 128, bar);
+        bulk_g2s(dst + c_wss * c_wb + j * 128, c_z + gi * 128, 128, bar);
       }
     }
     if (++islot == kGDepth) islot = 0;
@@ -454,12 +464,15 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
     // dispatch inside the loop, compile-time stage geometry
     auto stage_loop = [&](auto bits_c, auto gps_c) {
       constexpr int B = decltype(bits_c)::value, G = decltype(gps_c)::value;
-      constexpr int WB = B * 512, ZPJ = (G > 0 ? G : 1) * 128;
+      constexpr int WB = B * 512, ZPJ = (G > 0 ? G : 1) * 128, WSS = wss_for(B, G);
+      const int zpj = G > 0 || f.g ? ZPJ : 0;  // full column: one (s, z) block per stage
+      int sub = 0;
       for (int s = K0; s < K1; s += kGSS) {
         const int nss = min(kGSS, K1 - s);
         mbar_wait(&rfull[rslot], rph);
         if (active) {
-          mbar_wait(&full[wslot], wph);
+          // a weight stage spans WSS / kGSS record stages (sub = the part done)
+          if (sub == 0) mbar_wait(&full[wslot], wph);
           const unsigned char* stg = ring + wslot * kGSlot;
           const unsigned char* rec = rring + rslot * kRecSlot;
           if (pl.mode != 1) {
@@ -467,21 +480,26 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
             for (int j = 0; j < kGSS; ++j) {
               if (j < nss) {
                 uint4 w[B];
+                const int js = sub + j;
 #pragma unroll
-                for (int v = 0; v < B; ++v) w[v] = ((const uint4*)(stg + j * WB))[v * 32 + lane];
-                group_superstep<B, G>(w, (const float2*)(stg + kGSS * WB + j * ZPJ),
+                for (int v = 0; v < B; ++v) w[v] = ((const uint4*)(stg + js * WB))[v * 32 + lane];
+                group_superstep<B, G>(w, (const float2*)(stg + WSS * WB + js * zpj),
                                       rec + j * kRecBytes, yv);
               }
             }
           }
-          __syncwarp();
-          if (lane == 0 && !cdone) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_one(true);
-          }
-          if (++wslot == kGDepth) {
-            wslot = 0;
-            wph ^= 1u;
+          sub += kGSS;
+          if (sub == WSS || s + kGSS >= K1) {
+            sub = 0;
+            __syncwarp();
+            if (lane == 0 && !cdone) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              issue_one(true);
+            }
+            if (++wslot == kGDepth) {
+              wslot = 0;
+              wph ^= 1u;
+            }
           }
         }
         __syncwarp();
