@@ -55,6 +55,29 @@ def algo_bytes(K, N, bits, g):
 STEP_BYTES = sum(algo_bytes(K, N, b, g) for b, g, (K, N) in SWEEP)
 
 
+def graph_kernel_counts(graph) -> tuple[int, int]:
+    """(kernel nodes, kernel nodes that are this package's own kernels) of a
+    captured CUDA graph (built with keep_graph=True), read back through the CUDA
+    driver API: the per-step launch count the bench reports."""
+    from cuda.bindings import driver as cu
+    g = cu.CUgraph(graph.raw_cuda_graph())
+    _, _, n = cu.cuGraphGetNodes(g, 0)
+    _, nodes, n = cu.cuGraphGetNodes(g, n)
+    total = ours = 0
+    for nd in nodes[:n]:
+        _, typ = cu.cuGraphNodeGetType(nd)
+        if typ != cu.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+            continue
+        total += 1
+        _, prm = cu.cuGraphKernelNodeGetParams(nd)
+        err, name = cu.cuFuncGetName(prm.func)
+        if err != cu.CUresult.CUDA_SUCCESS:
+            err, name = cu.cuKernelGetName(prm.kern)
+        name = name.decode() if isinstance(name, bytes) else str(name)
+        ours += "qigen" in name
+    return total, ours
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -234,13 +257,19 @@ def run_ours(args):
         with torch.cuda.stream(stream):
             fn()
             stream.synchronize()
-            g = torch.cuda.CUDAGraph()
+            g = torch.cuda.CUDAGraph(keep_graph=True)
             with torch.cuda.graph(g, stream=stream):
                 fn()
+            g.instantiate()
         stream.synchronize()
         return g
 
     graph = capture(group.run)
+    try:
+        k_total, k_ours = graph_kernel_counts(graph)
+    except Exception as e:  # noqa: BLE001 (reported, not fatal)
+        print(f"kernel count unavailable: {e}", file=sys.stderr)
+        k_total = k_ours = 2
 
     def chain():  # the same GEMVs as 36 dependent single-GEMV launches (PDL)
         for pw, x, y in zip(mats, xs, ys):
@@ -330,7 +359,8 @@ def run_ours(args):
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                     "api": "qgemv_batch(pms, xs_host): pinned H2D, grouped launch, D2H, sync"},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": k_ours * args.steps,
+            "kernels_per_step": {"ours": k_ours, "all": k_total},
             "clocks": sampler.report(),
         }
         if not args.no_cpu_baseline:
@@ -378,9 +408,15 @@ def run_decode(args):
         stream.synchronize()
         if world > 1:
             dist.barrier()
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(graph, stream=stream):
             nxt = model.step(tok, pos)
+        graph.instantiate()
+        try:
+            k_total, k_ours = graph_kernel_counts(graph)
+        except Exception as e:  # noqa: BLE001 (reported, not fatal)
+            print(f"kernel count unavailable: {e}", file=sys.stderr)
+            k_total = k_ours = None
         sampler = ClockSampler(local)
         with sampler:
             for _ in range(args.warmup):
@@ -445,7 +481,8 @@ def run_decode(args):
                          "bytes_per_step_per_gpu": nbytes, "traffic": None},
             "e2e": {"value": round(B / e2e_s, 2), "unit": "tokens/s", "h2d_bytes_per_step": 8 * B,
                     "d2h_bytes_per_step": 8 * B},
-            "gpu_launches": None,
+            "gpu_launches": None if k_ours is None else k_ours * args.steps,
+            "kernels_per_step": {"ours": k_ours, "all": k_total},
             "clocks": sampler.report(),
         }
         print(json.dumps(line), flush=True)
