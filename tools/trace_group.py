@@ -39,3 +39,6 @@ for i, x in enumerate(t):
     d = en - st
     print(f"run {i}: start {st.min():7.2f}-{st.max():7.2f}  end {en.min():7.2f}-{en.max():7.2f}  "
           f"dur min/med/max {d.min():6.1f}/{np.median(d):6.1f}/{d.max():6.1f}")
+en = (t[1][:, 3] - t[1][:, 0].min()) / 1e3
+print("run 1 CTA end percentiles (us from first start): " +
+      " ".join(f"p{p}={np.percentile(en, p):.1f}" for p in (0, 10, 25, 50, 75, 90, 100)))
