@@ -87,7 +87,7 @@ struct GPlan {
   int nitems, first_dyn, dynamic;
   int64_t total_items;   // activation items (4 rows) of all GEMVs
   int count;
-  int mode;              // tuning: 1 = stream only (no compute)
+  int mode;              // tuning: &15 == 1 stream only (no compute); &32 early trigger
   unsigned long long* trace;  // optional per-CTA %globaltimer (entry, exit)
 };
 
@@ -152,8 +152,15 @@ __device__ __forceinline__ void group_prep_item(const GPlan& pl, const GDesc& d,
 // count), launched just before the grouped kernel (which prefetches weights
 // meanwhile and waits for it before reading records or claiming items).
 __global__ void __launch_bounds__(256) group_prep_kernel(const GPlan pl) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
+  // mode & 32: trigger the grouped launch before waiting, so its CTAs take SMs
+  // (and start their weight prefetch) as the previous launch's CTAs leave
+  if (pl.mode & 32) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+  }
   // the previous grouped launch has completed: re-arm the dynamic schedule
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && pl.dynamic)
     *pl.counter = pl.first_dyn;
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
           if (sub == 0) mbar_wait(&full[wslot], wph);
           const unsigned char* stg = ring + wslot * kGSlot;
           const unsigned char* rec = rring + rslot * kRecSlot;
-          if (pl.mode != 1) {
+          if ((pl.mode & 15) != 1) {
 #pragma unroll
             for (int j = 0; j < kGSS; ++j) {
               if (j < nss) {
@@ -736,7 +743,7 @@ extern "C" int qigen_debug_group_mode(int mode) {
 extern "C" int qigen_gemv_group_run(const qigen_gemv_group* g, void* stream) {
   QIGEN_CHECK_ARG(g, QIGEN_ERR_ARG, "null group");
   GPlan plan = g->plan;
-  plan.mode = g_group_mode & 15;
+  plan.mode = g_group_mode & 47;
   plan.trace = g_trace;
   cudaLaunchAttribute pa;
   pa.id = cudaLaunchAttributeProgrammaticStreamSerialization;
