@@ -456,6 +456,26 @@ def test_group_gemv_matches_single_gemv_and_sees_new_inputs(q):
         assert rel_err(y.cpu().numpy(), ys.cpu().numpy()) <= 2e-6
 
 
+def test_group_gemv_back_to_back_launches_early_trigger(q):
+    """Steps issued as plain stream launches, so each prep kernel is a
+    programmatic dependent of the previous grouped kernel, with and without the
+    prep kernel's early trigger (qigen_debug_group_mode(32)): every step must
+    see the previous one complete (records, schedule counter, zeroed split y)."""
+    from paper_2307_03738_b200 import _lib
+    specs = [(4096, 4096, 4, 128), (11008, 4096, 3, 64), (512, 256, 2, 32), (1024, 64, 4, None)]
+    grp, entries, refs = _group_cases(q, specs, seed=31)
+    try:
+        for mode in (0, 32):
+            _lib.lib().qigen_debug_group_mode(mode)
+            for _ in range(8):
+                grp.run()
+            torch.cuda.synchronize()
+            for (pw, x, y), r, spec in zip(entries, refs, specs):
+                assert rel_err(y[0].cpu().numpy(), r[0]) <= TOL, (mode, spec)
+    finally:
+        _lib.lib().qigen_debug_group_mode(0)
+
+
 def test_group_gemv_rejects_bad_input(q):
     from paper_2307_03738_b200.runtime import GemvGroup
     cm, *_ = _case(q, 512, 64, 4, 16)
