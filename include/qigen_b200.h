@@ -162,6 +162,13 @@ typedef struct qigen_gemv_group qigen_gemv_group;
 int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs, qigen_gemv_group** out);
 int qigen_gemv_group_run(const qigen_gemv_group* group, void* stream);
 int qigen_gemv_group_destroy(qigen_gemv_group* group);
+/* Host-buffer form of a group run, the blocking qgemv_batch round trip
+ * (SPEC.md:349-357 returns host results): x_bytes from pinned host x_host to
+ * x_dev (the device block the group's descriptors point into), the run, y_bytes
+ * from y_dev back to pinned host y_host, then a stream synchronize. */
+int qigen_gemv_group_run_host(const qigen_gemv_group* group, const void* x_host, void* x_dev,
+                              size_t x_bytes, const void* y_dev, void* y_host, size_t y_bytes,
+                              void* stream);
 
 /* ---- decode-step glue (LLaMA driver) ----------------------------------------- */
 

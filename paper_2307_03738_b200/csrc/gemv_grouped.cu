@@ -766,6 +766,19 @@ extern "C" int qigen_gemv_group_run(const qigen_gemv_group* g, void* stream) {
   return QIGEN_OK;
 }
 
+extern "C" int qigen_gemv_group_run_host(const qigen_gemv_group* g, const void* x_host,
+                                         void* x_dev, size_t x_bytes, const void* y_dev,
+                                         void* y_host, size_t y_bytes, void* stream) {
+  QIGEN_CHECK_ARG(g && x_host && x_dev && y_dev && y_host, QIGEN_ERR_ARG, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  QIGEN_CUDA_RET(cudaMemcpyAsync(x_dev, x_host, x_bytes, cudaMemcpyHostToDevice, st));
+  const int rc = qigen_gemv_group_run(g, stream);
+  if (rc != QIGEN_OK) return rc;
+  QIGEN_CUDA_RET(cudaMemcpyAsync(y_host, y_dev, y_bytes, cudaMemcpyDeviceToHost, st));
+  QIGEN_CUDA_RET(cudaStreamSynchronize(st));
+  return QIGEN_OK;
+}
+
 extern "C" int qigen_gemv_group_destroy(qigen_gemv_group* g) {
   if (!g) return QIGEN_OK;
   if (g->blob) cudaFree(g->blob);

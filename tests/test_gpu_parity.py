@@ -476,6 +476,32 @@ def test_group_gemv_back_to_back_launches_early_trigger(q):
         _lib.lib().qigen_debug_group_mode(0)
 
 
+def test_group_gemv_run_host_c_abi(q):
+    """qigen_gemv_group_run_host: pinned host x in, pinned host y out, one call."""
+    from paper_2307_03738_b200 import _lib
+    from paper_2307_03738_b200.runtime import GemvGroup
+    specs = [(1024, 512, 4, 64), (2048, 256, 2, None)]
+    rng = np.random.default_rng(41)
+    pws = [q.PanelWeights.from_codes(_case(q, K, N, b, g, seed=41 + i)[0])
+           for i, (K, N, b, g) in enumerate(specs)]
+    koff = np.cumsum([0] + [K for K, *_ in specs])
+    noff = np.cumsum([0] + [N for _, N, *_ in specs])
+    xd = torch.zeros(int(koff[-1]), device="cuda")
+    yd = torch.zeros(int(noff[-1]), device="cuda")
+    grp = GemvGroup([(pw, xd[koff[i]:koff[i + 1]], yd[noff[i]:noff[i + 1]])
+                     for i, pw in enumerate(pws)])
+    xh = torch.from_numpy(rng.normal(0, 1, int(koff[-1])).astype(np.float32)).pin_memory()
+    yh = torch.full((int(noff[-1]),), float("nan")).pin_memory()
+    _lib.call("qigen_gemv_group_run_host", grp._h, xh.data_ptr(), xd.data_ptr(), xh.numel() * 4,
+              yd.data_ptr(), yh.data_ptr(), yh.numel() * 4, torch.cuda.current_stream().cuda_stream)
+    for i, pw in enumerate(pws):
+        ref = pw.gemv(xh[koff[i]:koff[i + 1]].cuda()).cpu()
+        assert rel_err(yh[noff[i]:noff[i + 1]].numpy(), ref.numpy()) <= 2e-6
+    with pytest.raises(Exception):
+        _lib.call("qigen_gemv_group_run_host", grp._h, None, xd.data_ptr(), 4, yd.data_ptr(),
+                  yh.data_ptr(), 4, torch.cuda.current_stream().cuda_stream)
+
+
 def test_group_gemv_rejects_bad_input(q):
     from paper_2307_03738_b200.runtime import GemvGroup
     cm, *_ = _case(q, 512, 64, 4, 16)

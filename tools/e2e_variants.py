@@ -18,7 +18,7 @@ ref = q.qgemv_batch(pms, xs)
 b = next(iter(R._BATCHES.values()))
 torch.cuda.synchronize()
 
-def t(f, n=100):
+def t(f, n=400):
     for _ in range(5):
         f()
     torch.cuda.synchronize()
@@ -38,6 +38,16 @@ def fresh_out():
     return np.split(yh.numpy(), b.noff[1:-1])
 
 s = torch.cuda.current_stream()
+def torch_copies():  # the previous qgemv_batch host path: torch copies, slices
+    np.concatenate(xs, out=b.xh_np, casting="same_kind")
+    b.x.copy_(b.xh, non_blocking=True)
+    b.group.run()
+    yh = torch.empty(b.y.numel(), pin_memory=True)
+    yh.copy_(b.y, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    yv = yh.numpy()
+    return [yv[sl] for sl in b.yslices]
+
 def fresh_out_lean():
     np.concatenate(xs, out=b.xh_np)
     b.x.copy_(b.xh, non_blocking=True)
@@ -67,10 +77,11 @@ def kern_only():
 for name, f in [("qgemv_batch", lambda: q.qgemv_batch(pms, xs)), ("fresh_out", fresh_out),
                 ("fresh_out_lean", fresh_out_lean), ("shared_copy_out", shared_copy_out),
                 ("gpu_side_only", copies_and_kernels), ("kernels_only", kern_only),
-                ("qgemv_batch", lambda: q.qgemv_batch(pms, xs))]:
+                ("qgemv_batch", lambda: q.qgemv_batch(pms, xs)), ("torch_copies", torch_copies),
+                ("qgemv_batch", lambda: q.qgemv_batch(pms, xs)), ("torch_copies", torch_copies)]:
     us = t(f)
     print("%-16s %7.1f us" % (name, us))
-for f in (fresh_out, fresh_out_lean, shared_copy_out):
+for f in (fresh_out, fresh_out_lean, shared_copy_out, torch_copies):
     out = f()
     assert all(np.array_equal(a, r) for a, r in zip(out, ref)), f.__name__
 print("outputs identical")
