@@ -226,7 +226,7 @@ class GemvGroup:
     to x are seen by the next ``run()``.  ``run()`` is stream-ordered and
     graph-capturable."""
 
-    def __init__(self, entries):
+    def __init__(self, entries, *, pinned_x: bool = False):
         import ctypes
 
         from ._lib import GemvDesc
@@ -235,7 +235,8 @@ class GemvGroup:
         for i, (pw, x, y) in enumerate(entries):
             x2 = x.reshape(1, -1) if x.dim() == 1 else x
             y2 = y.reshape(1, -1) if y.dim() == 1 else y
-            if x2.dtype not in _DTYPES or x2.stride(1) != 1 or not x2.is_cuda:
+            x_ok = x2.is_cuda or (pinned_x and x2.is_pinned())  # pinned: read over PCIe
+            if x2.dtype not in _DTYPES or x2.stride(1) != 1 or not x_ok:
                 raise ConfigError("group x must be a CUDA f32/f16/bf16 tensor with unit stride")
             if y2.dtype != torch.float32 or y2.stride(1) != 1 or y2.shape != (x2.shape[0], pw.m):
                 raise ConfigError(f"group y must be float32 [{x2.shape[0]}, {pw.m}]")
@@ -336,20 +337,36 @@ class _Batch:
         self.y = torch.zeros(int(self.noff[-1]), device=dev)
         self.xh = torch.zeros(int(self.koff[-1])).pin_memory()
         self.xh_np = self.xh.numpy()
-        self.group = GemvGroup([(pw, self.x[self.koff[i]:self.koff[i + 1]],
-                                 self.y[self.noff[i]:self.noff[i + 1]])
-                                for i, pw in enumerate(self.pws)])
+        self._group = self._group_host = None
+
+    @property
+    def group(self) -> "GemvGroup":
+        """Grouped launch over device inputs (``x``), built on first use."""
+        if self._group is None:
+            self._group = GemvGroup([(pw, self.x[self.koff[i]:self.koff[i + 1]],
+                                      self.y[self.noff[i]:self.noff[i + 1]])
+                                     for i, pw in enumerate(self.pws)])
+        return self._group
+
+    @property
+    def group_host(self) -> "GemvGroup":
+        """Grouped launch whose prep kernel reads the pinned gather buffer
+        (``xh``) over PCIe: no H2D copy (tools/zc_exp.py: 218 vs 236-240 us per
+        call on the configs[1] sweep, identical outputs)."""
+        if self._group_host is None:
+            self._group_host = GemvGroup([(pw, self.xh[self.koff[i]:self.koff[i + 1]],
+                                           self.y[self.noff[i]:self.noff[i + 1]])
+                                          for i, pw in enumerate(self.pws)], pinned_x=True)
+        return self._group_host
 
 
 def _batch_host_run(b: "_Batch"):
-    """One H2D copy of the gathered inputs, the grouped launch, one D2H copy."""
-    b.x.copy_(b.xh, non_blocking=True)
-    b.group.run()
+    """The grouped launch reading the gathered inputs from pinned host memory
+    (zero-copy), one D2H copy of the results."""
+    b.group_host.run()
     # results land in a fresh pinned block (torch's caching host allocator:
     # no cudaHostAlloc after warm-up) that the returned views own, so no
-    # host-side copy out of a shared staging buffer is needed.  (The one-call C
-    # form, qigen_gemv_group_run_host, measured ~17 us slower per call from
-    # Python: tools/e2e_variants.py.)
+    # host-side copy out of a shared staging buffer is needed.
     yh = torch.empty(b.y.numel(), pin_memory=True)
     yh.copy_(b.y, non_blocking=True)
     torch.cuda.current_stream().synchronize()
@@ -365,8 +382,9 @@ def qgemv_batch(pms, xs):
     """Independent ``qgemv(pm_i, x_i)`` calls for a list of
     matrices, as ONE grouped GPU launch (``GemvGroup``).  ``xs``: per matrix an
     [n_i] activation vector (numpy / CPU tensor, or CUDA f32 tensor).  Host
-    inputs are staged through one pinned buffer (one H2D and one D2H copy per
-    call) and numpy results are returned (views of one fresh pinned block);
+    inputs are gathered into one pinned buffer that the grouped launch reads
+    over PCIe (zero-copy, no H2D copy); one D2H copy per call returns numpy
+    results (views of one fresh pinned block);
     device inputs give CUDA tensors.
     The grouped plan and staging buffers are cached per matrix list (the 8 most
     recently used lists)."""

@@ -1,0 +1,57 @@
+"""A/B: qgemv_batch's host path (pinned gather, H2D copy, grouped launch, D2H)
+vs the grouped kernel's prep reading the pinned gather buffer directly over
+PCIe (zero-copy x: no H2D copy).  Same box, interleaved."""
+import sys, time
+from pathlib import Path
+import numpy as np
+import torch
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2307_03738_b200 as q  # noqa: E402
+from paper_2307_03738_b200 import runtime as R  # noqa: E402
+SWEEP = [(b, g, shp) for shp in [(4096, 4096), (4096, 11008), (11008, 4096)]
+         for b in (2, 3, 4) for g in (32, 64, 128, None)]
+pms, xs = [], []
+for i, (b, g, (K, N)) in enumerate(SWEEP):
+    w = torch.randn(K, N, device="cuda") * 0.02
+    cm = q.quantize_matrix(w, q.QuantConfig(b, g))
+    pms.append(q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N))))
+    xs.append(np.random.default_rng(i).normal(0, 1, K).astype(np.float32))
+ref = q.qgemv_batch(pms, xs)
+b = next(iter(R._BATCHES.values()))
+yz = torch.zeros_like(b.y)
+gz = R.GemvGroup([(pw, b.xh[b.koff[i]:b.koff[i + 1]], yz[b.noff[i]:b.noff[i + 1]])
+                  for i, pw in enumerate(b.pws)], pinned_x=True)
+torch.cuda.synchronize()
+
+
+def t(f, n=400):
+    for _ in range(5):
+        f()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        f()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / n * 1e6
+
+
+def zero_copy():
+    np.concatenate(xs, out=b.xh_np, casting="same_kind")
+    gz.run()
+    yh = torch.empty(yz.numel(), pin_memory=True)
+    yh.copy_(yz, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    yv = yh.numpy()
+    return [yv[sl] for sl in b.yslices]
+
+
+def kern_zc():
+    gz.run()
+
+
+for name, f in [("qgemv_batch", lambda: q.qgemv_batch(pms, xs)), ("zero_copy_x", zero_copy),
+                ("kernels_zc", kern_zc), ("kernels", b.group.run)] * 2:
+    print("%-14s %7.1f us" % (name, t(f)), flush=True)
+out = zero_copy()
+assert all(np.array_equal(a, r) for a, r in zip(out, ref))
+print("outputs identical")
