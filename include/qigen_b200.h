@@ -144,6 +144,8 @@ int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, in
  * latency or split-K reduction sits between them.  Each descriptor has the
  * meaning of the qigen_gemv arguments (panel-layout weights, 1..2 activation
  * rows).  Pointers are captured at create time; run() may be graph-captured.
+ * x may point into page-locked host memory (device-accessible under UVA): the
+ * activation prep then reads it over PCIe instead of needing an H2D copy.
  * Results equal qigen_gemv's to f32 rounding (full-K reduction per column,
  * deterministic). */
 typedef struct {
