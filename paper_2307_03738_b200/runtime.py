@@ -17,6 +17,7 @@ and errors, backed by libqigen_b200:
 
 from __future__ import annotations
 
+import operator
 from dataclasses import dataclass
 
 import numpy as np
@@ -332,6 +333,7 @@ class _Batch:
         self.noff = np.cumsum([0] + [pw.m for pw in self.pws])
         # per-matrix slices of the result block (np.split costs ~1 us per piece)
         self.xshapes = [(pw.n,) for pw in self.pws]
+        self.xtypes = [np.ndarray] * len(self.pws)
         self.yslices = [slice(int(a), int(e)) for a, e in zip(self.noff[:-1], self.noff[1:])]
         self.x = torch.zeros(int(self.koff[-1]), device=dev)
         self.y = torch.zeros(int(self.noff[-1]), device=dev)
@@ -376,6 +378,8 @@ def _batch_host_run(b: "_Batch"):
 
 _BATCHES: dict = {}
 _MAX_BATCHES = 8
+_LAST = [None, None]  # (matrix list object, _Batch) of the previous call
+_SHAPE = operator.attrgetter("shape")
 
 
 def qgemv_batch(pms, xs):
@@ -390,14 +394,18 @@ def qgemv_batch(pms, xs):
     recently used lists)."""
     if len(pms) != len(xs) or not pms:
         raise ConfigError("qgemv_batch needs one activation vector per matrix")
-    key = tuple(map(id, pms))
-    b = _BATCHES.pop(key, None)
-    if b is None or any(p is not q for p, q in zip(b.pms, pms)):
-        b = _Batch(pms, _dev.require_cuda())  # fails loudly without a GPU
-    _BATCHES[key] = b  # most recently used last
-    while len(_BATCHES) > _MAX_BATCHES:  # bounded: plans pin their matrices and buffers
-        _BATCHES.pop(next(iter(_BATCHES)))
-    if [x.shape if type(x) is np.ndarray else None for x in xs] == b.xshapes:
+    b = _LAST[1]
+    # same matrix list as the previous call: it is already the most recently used
+    if not (_LAST[0] is pms and len(pms) == len(b.pms) and all(map(operator.is_, pms, b.pms))):
+        key = tuple(map(id, pms))
+        b = _BATCHES.pop(key, None)
+        if b is None or any(p is not q for p, q in zip(b.pms, pms)):
+            b = _Batch(pms, _dev.require_cuda())  # fails loudly without a GPU
+        _BATCHES[key] = b  # most recently used last
+        while len(_BATCHES) > _MAX_BATCHES:  # bounded: plans pin their matrices and buffers
+            _BATCHES.pop(next(iter(_BATCHES)))
+        _LAST[0], _LAST[1] = pms, b
+    if list(map(type, xs)) == b.xtypes and list(map(_SHAPE, xs)) == b.xshapes:
         # fast path: every x a host numpy vector of the right length
         np.concatenate(xs, out=b.xh_np, casting="same_kind")
         return _batch_host_run(b)

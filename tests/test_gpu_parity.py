@@ -522,6 +522,19 @@ def test_qgemv_batch_public_api(q):
         ys = q.qgemv_batch(pms, xs)
         for y, r in zip(ys, refs):
             assert rel_err(y, r) <= TOL
+    # the same list object, mutated in place: the new matrix is used
+    cm, codes, s, z, rng = _case(q, 1024, 512, 2, 64, seed=47)
+    pms[0] = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (1024, 512)))
+    refs[0] = orc.qgemv_reference(codes, s, z, xs[0])
+    ys = q.qgemv_batch(pms, xs)
+    for y, r in zip(ys, refs):
+        assert rel_err(y, r) <= TOL
+    # mixed host inputs (a CPU tensor and a float64 array) take the general path
+    xs2 = [torch.from_numpy(xs[0]), xs[1].astype(np.float64), xs[2]]
+    for y, r in zip(q.qgemv_batch(pms, xs2), refs):
+        assert rel_err(y, r) <= TOL
+    with pytest.raises(q.ConfigError):
+        q.qgemv_batch(pms, [xs[0], xs[1][:-1], xs[2]])
 
 
 @pytest.mark.parametrize("tokens", [1, 2, 3, 8])
