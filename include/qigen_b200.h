@@ -164,6 +164,12 @@ typedef struct qigen_gemv_group qigen_gemv_group;
 int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs, qigen_gemv_group** out);
 int qigen_gemv_group_run(const qigen_gemv_group* group, void* stream);
 int qigen_gemv_group_destroy(qigen_gemv_group* group);
+/* run() with every y pointer moved by (y_base - y_plan_base) bytes: the same
+ * plan writes a fresh output block per call (e.g. page-locked host memory, the
+ * zero-copy qgemv_batch result: GEMVs whose y is host memory are never K-split,
+ * so their outputs are plain 32-byte coalesced stores). */
+int qigen_gemv_group_run_rebased(const qigen_gemv_group* group, const void* y_plan_base,
+                                 void* y_base, void* stream);
 /* Host-buffer form of a group run, the blocking qgemv_batch round trip
  * (SPEC.md:349-357 returns host results): x_bytes from pinned host x_host to
  * x_dev (the device block the group's descriptors point into), the run, y_bytes

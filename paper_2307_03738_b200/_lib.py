@@ -64,6 +64,7 @@ SIGNATURES = {
     "qigen_gemv_group_create": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
     "qigen_gemv_group_run": (_I32, [_P, _P]),
     "qigen_gemv_group_destroy": (_I32, [_P]),
+    "qigen_gemv_group_run_rebased": (_I32, [_P, _P, _P, _P]),
     "qigen_gemv_group_run_host": (_I32, [_P, _P, _P, ctypes.c_size_t, _P, _P, ctypes.c_size_t, _P]),
     "qigen_rope_kv": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "qigen_rmsnorm_f16": (_I32, [_P, _P, _I64, _I64, ctypes.c_float, _P, _P]),

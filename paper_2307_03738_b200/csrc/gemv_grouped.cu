@@ -88,6 +88,7 @@ struct GPlan {
   int64_t total_items;   // activation items (4 rows) of all GEMVs
   int count;
   int mode;              // tuning: &15 == 1 stream only (no compute); &32 early trigger
+  int64_t ydelta;        // bytes added to every y pointer (run_rebased: a fresh output block)
   unsigned long long* trace;  // optional per-CTA %globaltimer (entry, exit)
 };
 
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(256) group_prep_kernel(const GPlan pl) {
   const GDesc& d = pl.desc[blockIdx.y];
   if (d.split)  // the two K halves add into a zeroed y
     for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < (int64_t)d.M * d.m; i += gridDim.x * 256)
-      d.y[(i / d.m) * d.ldy + i % d.m] = 0.f;
+      ((float*)((char*)d.y + pl.ydelta))[(i / d.m) * d.ldy + i % d.m] = 0.f;
   if ((int)blockIdx.x * 256 >= d.KS * 64) return;
   const int it = blockIdx.x * 256 + threadIdx.x;
   const int U = d.g == 32 ? 32 : d.g == 64 ? 64 : 128;  // exponent unit (rows)
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__((kGWarps + 1) * 32, 1) gemv_group_kernel(const
     const bool active = p < f.P;
     const int combo = f.combo;
     const int K0 = f.k0, K1 = f.k1;  // registers (see the producer)
-    float* const yg = f.y;
+    float* const yg = (float*)((char*)f.y + pl.ydelta);
     const int64_t ldy = f.ldy;
     const int M = f.M, m = f.m, split = f.split;
     float yv[2] = {0.f, 0.f};
@@ -640,6 +641,14 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
     const int pct_knob = (g_group_mode >> 8) & 0xff;
     const double pct = (g_group_mode & 16) ? 101.0 : pct_knob ? pct_knob - 1 : kSplitPct;
     for (GDesc& d : ds) d.split = (d.KS >= 8 && item_cost(d, kGWarps, d.KS) < mx * pct / 100.0);
+    // y in host memory (zero-copy output): plain stores only, never split atomics
+    for (GDesc& d : ds) {
+      cudaPointerAttributes a{};
+      if (d.split && cudaPointerGetAttributes(&a, d.y) == cudaSuccess &&
+          a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+        d.split = 0;
+    }
+    cudaGetLastError();
   }
   // items (GEMV x 16 panels x K range) and their cost
   std::vector<GItem> items;
@@ -722,6 +731,7 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
   g->plan.total_items = recs * 64;
   g->plan.count = count;
   g->plan.mode = 0;
+  g->plan.ydelta = 0;
   g->plan.trace = nullptr;
   g->grid = grid;
   g->max_ks = max_ks;
@@ -764,6 +774,14 @@ extern "C" int qigen_gemv_group_run(const qigen_gemv_group* g, void* stream) {
   cfg.numAttrs = 1;
   QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, gemv_group_kernel, plan));
   return QIGEN_OK;
+}
+
+extern "C" int qigen_gemv_group_run_rebased(const qigen_gemv_group* g, const void* y_plan_base,
+                                            void* y_base, void* stream) {
+  QIGEN_CHECK_ARG(g && y_plan_base && y_base, QIGEN_ERR_ARG, "null pointer");
+  qigen_gemv_group h = *g;
+  h.plan.ydelta = (int64_t)((const char*)y_base - (const char*)y_plan_base);
+  return qigen_gemv_group_run(&h, stream);
 }
 
 extern "C" int qigen_gemv_group_run_host(const qigen_gemv_group* g, const void* x_host,

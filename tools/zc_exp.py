@@ -53,5 +53,5 @@ for name, f in [("qgemv_batch", lambda: q.qgemv_batch(pms, xs)), ("zero_copy_x",
                 ("kernels_zc", kern_zc), ("kernels", b.group.run)] * 2:
     print("%-14s %7.1f us" % (name, t(f)), flush=True)
 out = zero_copy()
-assert all(np.array_equal(a, r) for a, r in zip(out, ref))
-print("outputs identical")
+assert all(np.allclose(a, r, rtol=1e-5, atol=1e-5) for a, r in zip(out, ref))  # split vs unsplit K: f32 rounding
+print("outputs match (1e-5)")
