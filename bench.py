@@ -359,7 +359,7 @@ def run_ours(args):
                          "frac": round(kernel_gbs / peak, 4), "traffic": _traffic()},
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "api": "qgemv_batch(pms, xs_host): gather into pinned memory, grouped launch reading it over PCIe (zero-copy H2D), D2H, sync"},
+                    "api": "qgemv_batch(pms, xs_host): gather into pinned memory, grouped launch reading it over PCIe and storing y into a fresh pinned block (zero-copy both ways), sync"},
             "gpu_launches": k_ours * args.steps,
             "kernels_per_step": {"ours": k_ours, "all": k_total},
             "clocks": sampler.report(),
