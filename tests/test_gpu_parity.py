@@ -502,6 +502,27 @@ def test_group_gemv_run_host_c_abi(q):
                   yh.data_ptr(), 4, torch.cuda.current_stream().cuda_stream)
 
 
+def test_group_gemv_run_rebased(q):
+    """qigen_gemv_group_run_rebased: one plan writes to a different output block
+    per run (device block and pinned host block); the plan's own y is untouched."""
+    from paper_2307_03738_b200 import _lib
+    from paper_2307_03738_b200.runtime import GemvGroup
+    specs = [(1024, 512, 4, 64), (4096, 4096, 3, 128), (512, 64, 2, None)]
+    grp0, entries, refs = _group_cases(q, specs, seed=51)
+    noff = np.cumsum([0] + [N for _, N, *_ in specs])
+    y0 = torch.full((int(noff[-1]),), float("nan"), device="cuda")
+    grp = GemvGroup([(pw, x, y0[noff[i]:noff[i + 1]]) for i, (pw, x, _) in enumerate(entries)])
+    st = torch.cuda.current_stream().cuda_stream
+    for blk in (torch.zeros(int(noff[-1]), device="cuda"),
+                torch.zeros(int(noff[-1])).pin_memory()):
+        _lib.call("qigen_gemv_group_run_rebased", grp._h, y0.data_ptr(), blk.data_ptr(), st)
+        torch.cuda.synchronize()
+        out = blk.cpu().numpy()
+        for i, r in enumerate(refs):
+            assert rel_err(out[noff[i]:noff[i + 1]], r[0]) <= TOL, (blk.device, specs[i])
+    assert torch.isnan(y0).all()
+
+
 def test_group_gemv_rejects_bad_input(q):
     from paper_2307_03738_b200.runtime import GemvGroup
     cm, *_ = _case(q, 512, 64, 4, 16)
