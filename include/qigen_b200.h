@@ -127,7 +127,13 @@ int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int b
  *     from the sums of squares of the x chunks (fixed reduction order).
  * workspace (device, >= qigen_gemv_workspace_size bytes, or NULL): scratch for the
  * activation digits when they are prepared once per call (long K chunks / many
- * tokens); NULL uses a grow-only library buffer that cannot grow during capture. */
+ * tokens).  NULL allocates that scratch stream-ordered for this call
+ * (cudaMallocFromPoolAsync / cudaFreeAsync on `stream`; a graph memory node
+ * under capture), so concurrent calls on different streams never share it; the
+ * stream-ordered free ends the programmatic-launch overlap with the next
+ * kernel, so hot paths pass a workspace.  Every GEMV entry point is re-entrant
+ * across streams and host threads: the only shared state is read-only
+ * (weights) or caller-owned (x, y, workspace). */
 int64_t qigen_gemv_workspace_size(int64_t n, int64_t tokens);
 int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
                   int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
@@ -144,8 +150,11 @@ int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, in
  * latency or split-K reduction sits between them.  Each descriptor has the
  * meaning of the qigen_gemv arguments (panel-layout weights, 1..2 activation
  * rows).  Pointers are captured at create time; run() may be graph-captured.
- * x may point into page-locked host memory (device-accessible under UVA): the
- * activation prep then reads it over PCIe instead of needing an H2D copy.
+ * x and y may point into page-locked host memory (device-accessible under UVA):
+ * the activation prep then reads x over PCIe instead of needing an H2D copy;
+ * pageable host memory is rejected (QIGEN_ERR_ARG).  A plan's activation
+ * records and schedule counter belong to the plan: run one plan on one stream
+ * at a time (different plans run concurrently).
  * Results equal qigen_gemv's to f32 rounding (full-K reduction per column,
  * deterministic). */
 typedef struct {
@@ -167,7 +176,9 @@ int qigen_gemv_group_destroy(qigen_gemv_group* group);
 /* run() with every y pointer moved by (y_base - y_plan_base) bytes: the same
  * plan writes a fresh output block per call (e.g. page-locked host memory, the
  * zero-copy qgemv_batch result: GEMVs whose y is host memory are never K-split,
- * so their outputs are plain 32-byte coalesced stores). */
+ * so their outputs are plain 32-byte coalesced stores).  QIGEN_ERR_ARG when
+ * y_base is pageable host memory, or host memory while the plan (created with
+ * device y) K-splits some GEMV. */
 int qigen_gemv_group_run_rebased(const qigen_gemv_group* group, const void* y_plan_base,
                                  void* y_base, void* stream);
 /* Host-buffer form of a group run, the blocking qgemv_batch round trip
@@ -217,6 +228,12 @@ int qigen_gemm_tc(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, in
                   float* y, int64_t ldy, int accumulate, int k_splits, void* workspace,
                   int64_t workspace_bytes, void* stream);
 
+/* ---- tuning / debugging aids ------------------------------------------------
+ * Not part of the product API: measurement knobs for tools/ and tests.  Each
+ * knob is PER CALLING HOST THREAD (thread-local): setting it changes only the
+ * launches that thread makes, never another thread's.  Defaults are the
+ * product settings. */
+
 /* Debugging aid: when buf is non-NULL every later qigen_gemv launch writes
  * %globaltimer stamps (entry, after the PDL wait, after the activation
  * prologue, after the main loop, exit, ...) to buf[(cta_y*grid_x + cta_x)*16 + i]. */
@@ -228,16 +245,14 @@ int qigen_debug_trace_clk(void* buf);
 int qigen_debug_prefetch(int stages_before_wait);
 /* Tuning aid: 1 = always digitise activations in the separate prep kernel. */
 int qigen_debug_force_prep(int on);
-/* Tuning aid: 1 = trigger the dependent launch (PDL) at GEMV kernel entry. */
 /* Tuning aid: cap the automatic K split (thread-block cluster size) of the GEMV. */
 int qigen_debug_max_split(int s);
-/* Tuning aid: preferred shared-memory carveout (percent, -1 = driver default) of the GEMV. */
-int qigen_debug_carveout(int pct);
 /* Tuning aid: 1 (default) = GEMVs with the RMSNorm prologue digitise through the
  * one-CTA-per-token prep kernel. */
 int qigen_debug_norm_prep(int on);
 /* Tuning aid: L2 evict_first on weight copies, warps per CTA (8/16), ring KB per CTA, grid cap. */
 int qigen_debug_gemv_tuning(int policy, int wpc, int ring_kb, int max_ctas);
+/* Tuning aid: 1 = trigger the dependent launch (PDL) at GEMV kernel entry. */
 int qigen_debug_early_trigger(int on);
 /* Tuning aid for the tensor-core path: 1 = skip A-tile stores, 2 = skip MMAs. */
 int qigen_debug_tc_mode(int mode);
@@ -265,7 +280,9 @@ int qigen_weights_destroy(qigen_weights* w);
 int qigen_weights_gemv(const qigen_weights* w, const void* x, int x_dtype, int64_t tokens,
                        float* y, int accumulate, void* stream);
 /* End-to-end call with HOST buffers: copies x_host in, runs the GEMV, copies
- * y_host out and synchronises `stream` (the reference-facing blocking call). */
+ * y_host out and synchronises `stream` (the reference-facing blocking call,
+ * SPEC.md:349-357).  Device staging is stream-ordered scratch, so one handle may
+ * serve several threads / streams concurrently. */
 int qigen_weights_gemv_host(const qigen_weights* w, const float* x_host, int64_t tokens,
                             float* y_host, void* stream);
 

@@ -59,7 +59,6 @@ SIGNATURES = {
     "qigen_gemv_ex": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64,
                              _I32, _I32, _I32, _P, ctypes.c_float, _P, _I64, _P]),
     "qigen_debug_max_split": (_I32, [_I32]),
-    "qigen_debug_carveout": (_I32, [_I32]),
     "qigen_debug_norm_prep": (_I32, [_I32]),
     "qigen_gemv_group_create": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
     "qigen_gemv_group_run": (_I32, [_P, _P]),

@@ -25,9 +25,6 @@ struct qigen_weights {
   int bits;
   uint32_t* qw;
   float* qsz;
-  float* x_dev;  // staging for qigen_weights_gemv_host
-  float* y_dev;
-  int64_t io_tokens;
 };
 
 extern "C" int qigen_weights_create(const uint32_t* words, int layout, int64_t n, int64_t m,
@@ -37,6 +34,18 @@ extern "C" int qigen_weights_create(const uint32_t* words, int layout, int64_t n
   QIGEN_CHECK_ARG(out && words && scales && zeros, QIGEN_ERR_ARG, "null pointer");
   QIGEN_CHECK_ARG(layout == QIGEN_LAYOUT_ROW_SEQUENTIAL || layout == QIGEN_LAYOUT_ZCURVE,
                   QIGEN_ERR_ARG, "unknown layout %d", layout);
+  // config.py:54-55,73-74,108-113 (ConfigError) before any allocation
+  QIGEN_CHECK_ARG(bits == 2 || bits == 3 || bits == 4, QIGEN_ERR_CONFIG,
+                  "bits must be one of (2, 3, 4), got %d", bits);
+  QIGEN_CHECK_ARG(n > 0 && m > 0, QIGEN_ERR_CONFIG, "matrix must be non-empty");
+  QIGEN_CHECK_ARG(group >= 0 && (group == 0 || n % group == 0), QIGEN_ERR_CONFIG,
+                  "group size %lld does not divide row count %lld", (long long)group,
+                  (long long)n);
+  QIGEN_CHECK_ARG(n % unit_codes(bits) == 0, QIGEN_ERR_CONFIG,
+                  "row count %lld is not a multiple of %d for %d-bit packing", (long long)n,
+                  unit_codes(bits), bits);
+  QIGEN_CHECK_ARG(layout != QIGEN_LAYOUT_ZCURVE || (blk_rc && nblk > 0 && m_b > 0 && t_b > 0),
+                  QIGEN_ERR_PACK, "ZCURVE words need the block table and the plan's (m_b, t_b)");
   cudaStream_t s = (cudaStream_t)stream;
   qigen_weights* w = (qigen_weights*)calloc(1, sizeof(qigen_weights));
   QIGEN_CHECK_ARG(w, QIGEN_ERR_ARG, "out of host memory");
@@ -77,8 +86,6 @@ extern "C" int qigen_weights_destroy(qigen_weights* w) {
   if (!w) return QIGEN_OK;
   if (w->qw) cudaFree(w->qw);
   if (w->qsz) cudaFree(w->qsz);
-  if (w->x_dev) cudaFree(w->x_dev);
-  if (w->y_dev) cudaFree(w->y_dev);
   free(w);
   return QIGEN_OK;
 }
@@ -90,24 +97,28 @@ extern "C" int qigen_weights_gemv(const qigen_weights* w, const void* x, int x_d
                     w->m, accumulate, 0, stream);
 }
 
-extern "C" int qigen_weights_gemv_host(const qigen_weights* wc, const float* x_host,
+extern "C" int qigen_weights_gemv_host(const qigen_weights* w, const float* x_host,
                                        int64_t tokens, float* y_host, void* stream) {
-  QIGEN_CHECK_ARG(wc && x_host && y_host, QIGEN_ERR_ARG, "null pointer");
-  qigen_weights* w = (qigen_weights*)wc;
+  QIGEN_CHECK_ARG(w && x_host && y_host, QIGEN_ERR_ARG, "null pointer");
+  QIGEN_CHECK_ARG(tokens >= 1, QIGEN_ERR_ARG, "tokens must be >= 1");
   cudaStream_t s = (cudaStream_t)stream;
-  if (w->io_tokens < tokens) {
-    if (w->x_dev) cudaFree(w->x_dev);
-    if (w->y_dev) cudaFree(w->y_dev);
-    w->x_dev = w->y_dev = nullptr;
-    QIGEN_CUDA_RET(cudaMalloc((void**)&w->x_dev, tokens * w->n * 4));
-    QIGEN_CUDA_RET(cudaMalloc((void**)&w->y_dev, tokens * w->m * 4));
-    w->io_tokens = tokens;
-  }
-  QIGEN_CUDA_RET(cudaMemcpyAsync(w->x_dev, x_host, tokens * w->n * 4, cudaMemcpyHostToDevice, s));
-  int st = qigen_gemv(w->qw, w->qsz, w->n, w->m, w->bits, w->group, w->x_dev, QIGEN_F32, tokens,
-                      w->n, w->y_dev, w->m, 0, 0, stream);
+  // device staging is stream-ordered scratch (not owned by the handle), so one
+  // handle may serve several host threads / streams at once (read-only weights)
+  const size_t xb = (size_t)tokens * w->n * 4, yb = (size_t)tokens * w->m * 4;
+  unsigned char* io = nullptr;
+  int st = scratch_alloc(s, (xb + 255) / 256 * 256 + yb, &io);
   if (st) return st;
-  QIGEN_CUDA_RET(cudaMemcpyAsync(y_host, w->y_dev, tokens * w->m * 4, cudaMemcpyDeviceToHost, s));
+  float* x_dev = (float*)io;
+  float* y_dev = (float*)(io + (xb + 255) / 256 * 256);
+  cudaError_t e = cudaMemcpyAsync(x_dev, x_host, xb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    st = qigen_gemv(w->qw, w->qsz, w->n, w->m, w->bits, w->group, x_dev, QIGEN_F32, tokens,
+                    w->n, y_dev, w->m, 0, 0, stream);
+    if (!st) e = cudaMemcpyAsync(y_host, y_dev, yb, cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(io, s);
+  if (st) return st;
+  QIGEN_CUDA_RET(e);
   QIGEN_CUDA_RET(cudaStreamSynchronize(s));
   return QIGEN_OK;
 }

@@ -3,12 +3,37 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/qigen_b200.h"
 
 namespace qigen {
 
 // Set by every C-ABI entry point that fails; read with qigen_last_error().
 void set_error(const char* fmt, ...);
+
+// Stream-ordered scratch (gemv.cu): released with cudaFreeAsync on the same
+// stream behind the kernels that use it; safe for concurrent streams.
+int scratch_alloc(cudaStream_t stream, size_t bytes, unsigned char** out);
+
+// Lazy per-device setup (kernel attributes) that is safe when several host
+// threads make their first call at once: fn runs exactly once per device, and
+// every caller sees its status.
+constexpr int kMaxDevices = 64;
+struct OncePerDevice {
+  std::once_flag flag[kMaxDevices];
+  int status[kMaxDevices] = {};
+  template <class F>
+  int run(F&& fn) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+      set_error("no current CUDA device");
+      return QIGEN_ERR_CUDA;
+    }
+    std::call_once(flag[dev], [&] { status[dev] = fn(); });
+    return status[dev];
+  }
+};
 
 #define QIGEN_CHECK_ARG(cond, code, ...)   \
   do {                                     \

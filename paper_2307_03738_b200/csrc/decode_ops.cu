@@ -295,13 +295,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const AttnArg
 
 using namespace qigen;
 
-static unsigned long long* g_attn_trace = nullptr;
-static int g_attn_carveout = -1;
-extern "C" int qigen_attn_set_carveout(int pct) {
-  g_attn_carveout = pct;
-  return QIGEN_OK;
-}
-static int g_attn_splits = 12;  // splits (cluster size) cap per head: 12 measured best at ctx 1025 (tools/attn_exp.py)
+// tuning aids: per calling thread (a knob set by one thread never changes
+// another thread's launches)
+static thread_local unsigned long long* g_attn_trace = nullptr;
+static thread_local int g_attn_splits = 12;  // splits (cluster size) cap per head: 12 measured best at ctx 1025 (tools/attn_exp.py)
 extern "C" int qigen_debug_attn_splits(int n) {
   g_attn_splits = n < 1 ? 1 : (n > kAttnMaxSplit ? kAttnMaxSplit : n);
   return QIGEN_OK;
@@ -352,21 +349,16 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
   a.out = out;
   a.trace = g_attn_trace;
   auto kern = head_dim == 128 ? attn_decode_kernel<128> : attn_decode_kernel<64>;
-  static int carveout = -2;
-  if (carveout != g_attn_carveout) {  // tuning aid (qigen_debug_carveout)
-    carveout = g_attn_carveout;
-    for (auto kf : {attn_decode_kernel<128>, attn_decode_kernel<64>})
-      QIGEN_CUDA_RET(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
-  }
-  static bool configured = false;
-  if (!configured) {
+  static OncePerDevice once;
+  const int cst = once.run([]() -> int {
     for (auto kf : {attn_decode_kernel<128>, attn_decode_kernel<64>}) {
       QIGEN_CUDA_RET(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           200 * 1024));
       QIGEN_CUDA_RET(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     }
-    configured = true;
-  }
+    return QIGEN_OK;
+  });
+  if (cst) return cst;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)a.nsplit, (unsigned)(batch * heads), 1);
   cfg.blockDim = dim3(kAttnThreads, 1, 1);

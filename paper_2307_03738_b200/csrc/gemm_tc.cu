@@ -32,8 +32,8 @@
 namespace cg = cooperative_groups;
 
 namespace qigen {
-extern unsigned long long* g_trace;
-static int g_tc_dbg = 0;
+extern thread_local unsigned long long* g_trace;
+static thread_local int g_tc_dbg = 0;  // tuning aid, per calling thread
 namespace tc {
 
 struct TcArgs {
@@ -546,12 +546,9 @@ __global__ void __launch_bounds__(kThreads, 1) qgemm_tc_kernel(const TcArgs a) {
 }
 
 int sm_count_tc() {
-  static int c = 0;
-  if (!c) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, d);
-  }
+  int d = 0, c = 148;
+  cudaGetDevice(&d);
+  cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, d);
   return c;
 }
 
@@ -559,13 +556,14 @@ template <int GPS, int NT>
 static int launch(TcArgs& a, int req_S, void* ws, cudaStream_t stream, const void* x, int dtype,
                   int64_t ldx) {
   auto kern = qgemm_tc_kernel<GPS, NT>;
-  static bool configured = false;
-  if (!configured) {
+  static OncePerDevice once;
+  const int cst = once.run([&]() -> int {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
-  }
+    return QIGEN_OK;
+  });
+  if (cst) return cst;
   const int cols = (a.P + kPanels - 1) / kPanels;
   int S = req_S;
   if (S <= 0) {  // about one CTA per SM, at most 8 per cluster

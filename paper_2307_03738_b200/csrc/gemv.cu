@@ -608,54 +608,62 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-unsigned long long* g_trace = nullptr;  // shared with gemm_tc.cu
-static unsigned long long* g_trace_clk = nullptr;
+// Tuning / debugging aids (qigen_debug_*): per calling thread, so a knob set by
+// one thread never changes another thread's launches.  The product defaults
+// are the initial values.
+thread_local unsigned long long* g_trace = nullptr;  // shared with gemm_tc.cu, gemv_grouped.cu
+static thread_local unsigned long long* g_trace_clk = nullptr;
 constexpr int kMaxSplits = 16;  // cluster size along K (non-portable above 8)
-static int g_pre = -1;  // stages issued before the PDL wait (-1: all of the first fill)
-static int g_force_prep = 0;  // tuning: always digitise activations in act_prep_kernel
-static int g_early = 0;       // tuning: trigger the dependent launch at kernel entry
-static int g_policy = 0;      // tuning: L2 evict_first hint on weight copies
-static int g_wpc = 8;         // tuning: warps per CTA for <= 4 tokens (8 or 16)
-static int g_ring_kb = 0;     // tuning: ring bytes per CTA (KB; 0 = 10 KB per warp)
-static int g_max_ctas = 0;    // tuning: cap on the grid (0 = rule below)
-static int g_max_split = kMaxSplits;  // tuning: cap on the automatic K split (cluster size)
-static int g_carveout = -1;           // tuning: preferred shared-memory carveout (-1: default)
-}  // namespace qigen
-extern "C" int qigen_attn_set_carveout(int pct);  // decode_ops.cu
-namespace qigen {
-static int g_norm_prep = 1;           // RMSNorm prologues via act_prep_norm_kernel (measured: -1 us per 7B layer)
+static thread_local int g_pre = -1;  // stages issued before the PDL wait (-1: all of the first fill)
+static thread_local int g_force_prep = 0;  // always digitise activations in act_prep_kernel
+static thread_local int g_early = 0;       // trigger the dependent launch at kernel entry
+static thread_local int g_policy = 0;      // L2 evict_first hint on weight copies
+static thread_local int g_wpc = 8;         // warps per CTA for <= 4 tokens (8 or 16)
+static thread_local int g_ring_kb = 0;     // ring bytes per CTA (KB; 0 = 10 KB per warp)
+static thread_local int g_max_ctas = 0;    // cap on the grid (0 = rule below)
+static thread_local int g_max_split = kMaxSplits;  // cap on the automatic K split (cluster size)
+static thread_local int g_norm_prep = 1;  // RMSNorm prologues via act_prep_norm_kernel (measured: -1 us per 7B layer)
 
 static int sm_count() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
 }
 
-// Grow-only per-device fallback workspace for prepared activation digits (used
-// when the caller passes none).  Growing is not allowed during stream capture.
-static int fallback_workspace(cudaStream_t stream, size_t bytes, unsigned char** out) {
-  static std::unordered_map<int, std::pair<unsigned char*, size_t>> ws;
+// Scratch for prepared activation digits when the caller passes no workspace:
+// allocated stream-ordered for this call and freed stream-ordered behind its
+// kernels, so concurrent calls on different streams (or threads) never share
+// it.  Outside capture it comes from a per-device pool that keeps its memory
+// (no cudaMalloc after warm-up); inside stream capture it becomes a graph
+// memory node.  Callers on a hot path pass a workspace instead
+// (qigen_gemv_workspace_size): the free is a full stream dependency, which
+// ends the programmatic-launch overlap with the next kernel.
+int scratch_alloc(cudaStream_t stream, size_t bytes, unsigned char** out) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  QIGEN_CUDA_RET(cudaStreamIsCapturing(stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    QIGEN_CUDA_RET(cudaMallocAsync((void**)out, bytes, stream));
+    return QIGEN_OK;
+  }
+  static std::once_flag flag[kMaxDevices];
+  static cudaMemPool_t pool[kMaxDevices];
+  static int pst[kMaxDevices];
   int dev = 0;
   QIGEN_CUDA_RET(cudaGetDevice(&dev));
-  auto& e = ws[dev];
-  if (e.second < bytes) {
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &cap);
-    QIGEN_CHECK_ARG(cap == cudaStreamCaptureStatusNone, QIGEN_ERR_ARG,
-                    "GEMV workspace must grow outside stream capture: pass a workspace "
-                    "(qigen_gemv_workspace_size) or run this shape once before capturing");
-    if (e.first) QIGEN_CUDA_RET(cudaFree(e.first));
-    e.first = nullptr;
-    e.second = 0;
-    QIGEN_CUDA_RET(cudaMalloc((void**)&e.first, bytes));
-    e.second = bytes;
-  }
-  *out = e.first;
+  QIGEN_CHECK_ARG(dev >= 0 && dev < kMaxDevices, QIGEN_ERR_CUDA, "device index %d", dev);
+  std::call_once(flag[dev], [&] {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    uint64_t keep = ~0ull;
+    if (cudaMemPoolCreate(&pool[dev], &props) != cudaSuccess ||
+        cudaMemPoolSetAttribute(pool[dev], cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess)
+      pst[dev] = QIGEN_ERR_CUDA;
+  });
+  QIGEN_CHECK_ARG(!pst[dev], QIGEN_ERR_CUDA, "could not create the GEMV scratch pool");
+  QIGEN_CUDA_RET(cudaMallocFromPoolAsync((void**)out, bytes, pool[dev], stream));
   return QIGEN_OK;
 }
 
@@ -665,19 +673,14 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   constexpr int TP = 2 * NB;
   constexpr int UPS = GPS > 2 ? GPS : 2;
   constexpr int IPU = (8 / UPS) * 8;
-  static bool configured = false;
-  if (!configured) {
+  static OncePerDevice once;
+  const int cst = once.run([&]() -> int {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
-  }
-  static int carveout = -2;
-  if (carveout != g_carveout) {  // tuning aid: shared-memory carveout preference
-    carveout = g_carveout;
-    QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        carveout));
-  }
+    return QIGEN_OK;
+  });
+  if (cst) return cst;
   const int stage = BITS * 512 + GPS * 128;
   auto shape = [&](int S) {  // smem plan for S chunks: ring of <= 80 KB per CTA
     const int max_ks = (a.KS + S - 1) / S;
@@ -766,6 +769,7 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   // block, else once per GEMV in act_prep_kernel
   const int rounds = (a.M * a.max_steps * 8 + WPC * 32 - 1) / (WPC * 32);
   a.dig = nullptr;
+  unsigned char* scratch = nullptr;  // stream-ordered, freed behind this call's kernels
   // RMSNorm prologue for 1-2 tokens: one prep CTA per token (measured faster
   // than every CTA re-reading the row on the 7B chain; slower at 8 tokens)
   const bool norm_prep = a.xmode == 1 && a.M <= 2 && a.KS * 64 <= kNormPrepThreads * kNormPrepMaxR &&
@@ -775,8 +779,9 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     if (a.ws && a.ws_bytes >= bytes) {
       a.dig = a.ws;
     } else {
-      int st = fallback_workspace(stream, bytes, &a.dig);
+      int st = scratch_alloc(stream, bytes, &scratch);
       if (st) return st;
+      a.dig = scratch;
     }
     cudaLaunchConfig_t pc = {};
     pc.gridDim = dim3((unsigned)((a.KS * 64 + 255) / 256), (unsigned)TP, 1);
@@ -787,21 +792,16 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
     pa.val.programmaticStreamSerializationAllowed = 1;
     pc.attrs = &pa;
     pc.numAttrs = 1;
-    static int prep_carveout = -2;
-    if (prep_carveout != g_carveout) {  // tuning aid: same carveout as the GEMV
-      prep_carveout = g_carveout;
-      QIGEN_CUDA_RET(cudaFuncSetAttribute(act_prep_kernel<IPU>,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout));
-      QIGEN_CUDA_RET(cudaFuncSetAttribute(act_prep_norm_kernel<IPU>,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout));
-    }
+    cudaError_t pe;
     if (norm_prep) {
       pc.gridDim = dim3(1, (unsigned)TP, 1);
       pc.blockDim = dim3(kNormPrepThreads, 1, 1);
-      QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_norm_kernel<IPU>, a, (int)TP, (int)UPS));
+      pe = cudaLaunchKernelEx(&pc, act_prep_norm_kernel<IPU>, a, (int)TP, (int)UPS);
     } else {
-      QIGEN_CUDA_RET(cudaLaunchKernelEx(&pc, act_prep_kernel<IPU>, a, (int)TP, (int)UPS));
+      pe = cudaLaunchKernelEx(&pc, act_prep_kernel<IPU>, a, (int)TP, (int)UPS);
     }
+    if (pe != cudaSuccess && scratch) cudaFreeAsync(scratch, stream);
+    QIGEN_CUDA_RET(pe);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cols, (unsigned)S, 1);
@@ -822,7 +822,9 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, kern, a));
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, a);
+  if (scratch) QIGEN_CUDA_RET(cudaFreeAsync(scratch, stream));
+  QIGEN_CUDA_RET(le);
   return QIGEN_OK;
 }
 
@@ -866,12 +868,6 @@ extern "C" int qigen_debug_prefetch(int stages_before_wait) {
 
 extern "C" int qigen_debug_norm_prep(int on) {
   g_norm_prep = on;
-  return QIGEN_OK;
-}
-
-extern "C" int qigen_debug_carveout(int pct) {
-  g_carveout = pct;
-  qigen_attn_set_carveout(pct);
   return QIGEN_OK;
 }
 

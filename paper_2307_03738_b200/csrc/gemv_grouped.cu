@@ -42,7 +42,7 @@
 
 namespace qigen {
 
-extern unsigned long long* g_trace;  // gemv.cu (qigen_debug_trace)
+extern thread_local unsigned long long* g_trace;  // gemv.cu (qigen_debug_trace)
 
 constexpr int kGWarps = 16;            // consumer warps per CTA (panels per item)
 constexpr int kGTP = 2;                // tokens in the fragment layout (M <= 2)
@@ -565,16 +565,30 @@ constexpr int kGSmem = kGWarps * kGDepth * kGSlot + kGRecDepth * kRecSlot +
 
 using namespace qigen;
 
-// tuning: 1 stream only; at create: 16 split every K in two, (pct+1) << 8 sets
-// the split threshold (1 << 8: never split)
-static int g_group_mode = 0;
+// tuning aid (per calling thread): 1 stream only; at create: 16 split every K
+// in two, (pct+1) << 8 sets the split threshold (1 << 8: never split)
+static thread_local int g_group_mode = 0;
 
 struct qigen_gemv_group {
   void* blob = nullptr;  // device: descs | items | cta_start
   unsigned char* rec = nullptr;
   GPlan plan{};
   int grid = 0, max_ks = 0;
+  bool any_split = false;  // some GEMV adds two K halves into y with atomics
 };
+
+// Kind of memory behind p: device (or managed), page-locked host, or -1 for
+// memory the GPU cannot address (pageable host).
+static int mem_kind(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return 0;
+  if (a.type == cudaMemoryTypeHost) return 1;
+  return -1;
+}
 
 extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
                                        qigen_gemv_group** out) {
@@ -599,6 +613,10 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
                     "gemv %d: the grouped GEMV takes 1 or 2 activation rows", i);
     QIGEN_CHECK_ARG(e.x_dtype >= 0 && e.x_dtype <= 2, QIGEN_ERR_ARG, "gemv %d: bad x dtype", i);
     QIGEN_CHECK_ARG(e.ldx >= e.n && e.ldy >= e.m, QIGEN_ERR_ARG, "gemv %d: leading dimensions", i);
+    // x and y may be device or page-locked host memory (zero-copy over PCIe);
+    // pageable host memory would fault inside the kernel
+    QIGEN_CHECK_ARG(mem_kind(e.x) >= 0 && mem_kind(e.y) >= 0, QIGEN_ERR_ARG,
+                    "gemv %d: x and y must be device or page-locked host memory", i);
     GDesc& d = ds[i];
     d.qw = (const uint4*)e.qw;
     d.qsz = (const float2*)e.qsz;
@@ -642,13 +660,8 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
     const double pct = (g_group_mode & 16) ? 101.0 : pct_knob ? pct_knob - 1 : kSplitPct;
     for (GDesc& d : ds) d.split = (d.KS >= 8 && item_cost(d, kGWarps, d.KS) < mx * pct / 100.0);
     // y in host memory (zero-copy output): plain stores only, never split atomics
-    for (GDesc& d : ds) {
-      cudaPointerAttributes a{};
-      if (d.split && cudaPointerGetAttributes(&a, d.y) == cudaSuccess &&
-          a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
-        d.split = 0;
-    }
-    cudaGetLastError();
+    for (GDesc& d : ds)
+      if (d.split && mem_kind(d.y) != 0) d.split = 0;
   }
   // items (GEMV x 16 panels x K range) and their cost
   std::vector<GItem> items;
@@ -735,11 +748,16 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
   g->plan.trace = nullptr;
   g->grid = grid;
   g->max_ks = max_ks;
-  static bool configured = false;
-  if (!configured) {
+  for (const GDesc& d : ds) g->any_split = g->any_split || d.split;
+  static OncePerDevice once;
+  const int cst = once.run([]() -> int {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(gemv_group_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kGSmem));
-    configured = true;
+    return QIGEN_OK;
+  });
+  if (cst) {
+    qigen_gemv_group_destroy(g);
+    return cst;
   }
   *out = g;
   return QIGEN_OK;
@@ -779,6 +797,14 @@ extern "C" int qigen_gemv_group_run(const qigen_gemv_group* g, void* stream) {
 extern "C" int qigen_gemv_group_run_rebased(const qigen_gemv_group* g, const void* y_plan_base,
                                             void* y_base, void* stream) {
   QIGEN_CHECK_ARG(g && y_plan_base && y_base, QIGEN_ERR_ARG, "null pointer");
+  // the outputs move to y_base's memory: it must be GPU-addressable, and a plan
+  // whose K-split GEMVs add into y with atomics must not be moved to host memory
+  const int kind = mem_kind(y_base);
+  QIGEN_CHECK_ARG(kind >= 0, QIGEN_ERR_ARG,
+                  "y_base must be device or page-locked host memory");
+  QIGEN_CHECK_ARG(kind == 0 || !g->any_split, QIGEN_ERR_ARG,
+                  "this plan K-splits some GEMVs (atomic adds into y): y_base must be device "
+                  "memory; create the plan with host y to run it on host blocks");
   qigen_gemv_group h = *g;
   h.plan.ydelta = (int64_t)((const char*)y_base - (const char*)y_plan_base);
   return qigen_gemv_group_run(&h, stream);

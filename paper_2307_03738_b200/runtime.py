@@ -18,6 +18,7 @@ and errors, backed by libqigen_b200:
 from __future__ import annotations
 
 import operator
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,7 +34,6 @@ _DTYPES = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
 MAX_GEMV_TOKENS = 16
 TC_MIN_TOKENS = 16   # north_star (c): tensor cores only from 16 tokens up
 MAX_TC_TOKENS = 256
-TC_ENABLED = [True]  # tests flip this to compare against the GEMV path
 
 
 @dataclass
@@ -148,7 +148,7 @@ class PanelWeights:
 
     def _tc_ok(self) -> bool:
         g = self.config.group_size
-        return self.bits == 4 and g in (32, 64, 128, 256) and TC_ENABLED[0]
+        return self.bits == 4 and g in (32, 64, 128, 256)
 
     def nbytes_algorithmic(self) -> int:
         """Packed codes + f32 scale + f32 zero (the roofline bytes)."""
@@ -157,8 +157,13 @@ class PanelWeights:
 
     def gemv(self, x: torch.Tensor, out: torch.Tensor | None = None, *, accumulate: bool = False,
              k_splits: int = 0, prologue: str | None = None, norm_weight: torch.Tensor | None = None,
-             eps: float = 1e-5, x_ready: bool = False) -> torch.Tensor:
+             eps: float = 1e-5, x_ready: bool = False, path: str = "auto") -> torch.Tensor:
         """y[t, :] = f(x[t, :]) @ W for t < tokens; x: CUDA [tokens, n] or [n].
+
+        ``path``: ``"auto"`` (tensor-core GEMM from 16 tokens on when the
+        config allows it, north_star (c); the exact IMMA GEMV below),
+        ``"gemv"`` (always the IMMA GEMV) or ``"tc"`` (always the tensor-core
+        GEMM; 4-bit, g in 32..256).
 
         ``prologue`` fuses the producer-side glue into the GEMV: None (f = id),
         ``"rmsnorm"`` (f = RMSNorm with ``norm_weight``), ``"rmsnorm_folded"``
@@ -190,8 +195,15 @@ class PanelWeights:
         y2 = out.reshape(T, self.m) if out.dim() == 1 else out
         if y2.dtype != torch.float32 or y2.stride(1) != 1:
             raise ConfigError("out must be float32 with unit column stride")
+        if path not in ("auto", "gemv", "tc"):
+            raise ConfigError(f"path must be 'auto', 'gemv' or 'tc', got {path!r}")
+        if path == "tc" and (mode != 0 or not self._tc_ok()):
+            raise ConfigError("the tensor-core path takes 4-bit weights, g in (32, 64, 128, 256) "
+                              "and no prologue")
         st = _dev.stream_handle()
-        if T >= TC_MIN_TOKENS and mode == 0 and self._tc_ok():
+        use_tc = path == "tc" or (path == "auto" and T >= TC_MIN_TOKENS and mode == 0
+                                  and self._tc_ok())
+        if use_tc:
             # small-batch GEMM on the tcgen05 tensor cores (north_star (c))
             for t0 in range(0, T, MAX_TC_TOKENS):
                 t1 = min(T, t0 + MAX_TC_TOKENS)
@@ -239,8 +251,11 @@ class GemvGroup:
             x_ok = x2.is_cuda or (pinned_x and x2.is_pinned())  # pinned: read over PCIe
             if x2.dtype not in _DTYPES or x2.stride(1) != 1 or not x_ok:
                 raise ConfigError("group x must be a CUDA f32/f16/bf16 tensor with unit stride")
+            y_ok = y2.is_cuda or y2.is_pinned()  # pinned: stored over PCIe (zero-copy)
             if y2.dtype != torch.float32 or y2.stride(1) != 1 or y2.shape != (x2.shape[0], pw.m):
                 raise ConfigError(f"group y must be float32 [{x2.shape[0]}, {pw.m}]")
+            if not y_ok:
+                raise ConfigError("group y must be a CUDA tensor or pinned host memory")
             if x2.shape[1] != pw.n:
                 raise ConfigError(f"x has {x2.shape[1]} columns, expected {pw.n}")
             descs[i] = GemvDesc(pw.qw.data_ptr(), pw.qsz.data_ptr(), pw.n, pw.m, pw.bits,
@@ -340,6 +355,10 @@ class _Batch:
         self.xh = torch.zeros(int(self.koff[-1])).pin_memory()
         self.xh_np = self.xh.numpy()
         self._group = self._group_host = None
+        # the staging buffers, the plans' activation records and schedule
+        # counter are per list: concurrent calls on one list take turns
+        self.lock = threading.Lock()
+        self.done = None  # event after the last device-path call (other streams wait on it)
 
     @property
     def group(self) -> "GemvGroup":
@@ -391,13 +410,24 @@ def qgemv_batch(pms, xs):
     matrices, as ONE grouped GPU launch (``GemvGroup``).  ``xs``: per matrix an
     [n_i] activation vector (numpy / CPU tensor, or CUDA f32 tensor).  Host
     inputs are gathered into one pinned buffer that the grouped launch reads
-    over PCIe (zero-copy, no H2D copy); one D2H copy per call returns numpy
-    results (views of one fresh pinned block);
-    device inputs give CUDA tensors.
-    The grouped plan and staging buffers are cached per matrix list (the 8 most
-    recently used lists)."""
+    over PCIe, and the kernel stores y straight into a fresh pinned block
+    (zero-copy both ways: no H2D or D2H copy); the numpy results are views of
+    that block, so they stay valid across later calls.  Device inputs give
+    CUDA tensors.  The grouped plan and staging buffers are cached per matrix
+    list (the 8 most recently used lists); concurrent calls from several
+    threads are safe (calls on the same list are serialised)."""
     if len(pms) != len(xs) or not pms:
         raise ConfigError("qgemv_batch needs one activation vector per matrix")
+    with _CACHE_LOCK:
+        b = _lookup_batch(pms)
+    with b.lock:
+        return _batch_call(b, xs)
+
+
+_CACHE_LOCK = threading.Lock()
+
+
+def _lookup_batch(pms) -> "_Batch":
     b = _LAST[1]
     # same matrix list as the previous call: it is already the most recently used
     if not (_LAST[0] is pms and len(pms) == len(b.pms) and all(map(operator.is_, pms, b.pms))):
@@ -409,6 +439,12 @@ def qgemv_batch(pms, xs):
         while len(_BATCHES) > _MAX_BATCHES:  # bounded: plans pin their matrices and buffers
             _BATCHES.pop(next(iter(_BATCHES)))
         _LAST[0], _LAST[1] = pms, b
+    return b
+
+
+def _batch_call(b: "_Batch", xs):
+    if len(xs) != len(b.pws):
+        raise ConfigError("qgemv_batch needs one activation vector per matrix")
     if list(map(type, xs)) == b.xtypes and list(map(_SHAPE, xs)) == b.xshapes:
         # fast path: every x a host numpy vector of the right length
         np.concatenate(xs, out=b.xh_np, casting="same_kind")
@@ -428,13 +464,21 @@ def qgemv_batch(pms, xs):
             raise ConfigError(f"x[{i}] has shape {tuple(x.shape)}, expected [{pw.n}]")
         hx.append(x)
     if host:
-        # one host-side gather into the pinned staging buffer, one H2D copy,
-        # the grouped launch, one D2H copy
+        # one host-side gather into the pinned staging buffer, then the
+        # zero-copy grouped launch
         np.concatenate(hx, out=b.xh_np, casting="same_kind")
         return _batch_host_run(b)
+    # device path: stream-ordered, no host sync; a call on another stream
+    # first waits for the previous call's use of the shared buffers
+    cur = torch.cuda.current_stream()
+    if b.done is not None:
+        cur.wait_event(b.done)
     torch.cat([x.reshape(-1).float() for x in xs], out=b.x)
     b.group.run()
-    return list(torch.split(b.y.clone(), [pw.m for pw in b.pws]))
+    out = list(torch.split(b.y.clone(), [pw.m for pw in b.pws]))
+    b.done = torch.cuda.Event()
+    b.done.record(cur)
+    return out
 
 
 def qgemv_reference(pm, x):

@@ -42,12 +42,18 @@ TINY = D.LlamaConfig(n_layers=2, d_model=128, n_heads=4, head_dim=32, ffn=512, v
                      bits=4, group=32)
 
 
-def _run(rank, world, port, q):
+# uneven shards at TP 4, like 7B down_proj: ffn 1280 = 5 supersteps
+# of 256 -> K-shards 512/256/256/256; vocab 160 = 10 panels -> 48/48/32/32
+UNEVEN = D.LlamaConfig(n_layers=2, d_model=128, n_heads=4, head_dim=32, ffn=1280, vocab=160,
+                       bits=4, group=32)
+
+
+def _run(rank, world, port, q, cfg=TINY):
     from decode_backends import OracleBackend
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.manual_seed(0)
-    m = D.LlamaTP(TINY, batch=2, max_ctx=16, seed=3, device="cpu", tp=D.TP(),
+    m = D.LlamaTP(cfg, batch=2, max_ctx=16, seed=3, device="cpu", tp=D.TP(),
                   backend=OracleBackend, kv_dtype=torch.float32)
     tok = m.step(torch.tensor([5, 17]), pos=8)
     if rank == 0:
@@ -64,18 +70,25 @@ def _free_port():
     return p
 
 
-def test_tp2_matches_tp1_on_cpu():
+@pytest.mark.parametrize("world,cfg", [(2, TINY), (2, UNEVEN), (4, UNEVEN)])
+def test_tp_matches_tp1_on_cpu(world, cfg):
+    """TP=world on gloo (one process per rank) against TP=1: same greedy
+    tokens, logits within 1e-5; the uneven config exercises unequal K-shards of
+    the row-parallel down_proj and unequal vocab shards (padded all-gather)."""
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parent))
     from decode_backends import OracleBackend
-    ref = D.LlamaTP(TINY, batch=2, max_ctx=16, seed=3, device="cpu", backend=OracleBackend,
+    if cfg is UNEVEN and world == 4:
+        cuts = [D.row_shard(cfg.ffn, cfg.group, 4, r) for r in range(4)]
+        assert [hi - lo for lo, hi in cuts] == [512, 256, 256, 256]
+    ref = D.LlamaTP(cfg, batch=2, max_ctx=16, seed=3, device="cpu", backend=OracleBackend,
                     kv_dtype=torch.float32)
     tok1 = ref.step(torch.tensor([5, 17]), pos=8)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, q, cfg)) for r in range(world)]
     for p in procs:
         p.start()
     tok2, logits2 = q.get(timeout=300)
@@ -85,6 +98,29 @@ def test_tp2_matches_tp1_on_cpu():
     l1 = ref.last_logits.numpy()
     assert tok2 == tok1.tolist()
     assert abs(logits2 - l1).max() / (1 + abs(l1).max()) < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,B", [("7b", 1), ("65b", 8)])
+def test_gpu_full_width_layer_vs_oracle(name, B):
+    """One full-width layer of the BASELINE decode configs (7B: 4-bit g128,
+    d 4096, FFN 11008, KV 512; 65B: 3-bit g64, d 8192, FFN 22016, KV 1024, batch
+    8) plus the full 32000 vocab: the GPU step against the same model on the
+    oracle backend (CPU-oracle quantization, fp64 dense linears)."""
+    from decode_backends import OracleBackend
+    base, ctx = (D.LLAMA_7B, 512) if name == "7b" else (D.LLAMA_65B, 1024)
+    cfg = D.shrink(base, n_layers=1)
+    tok = (torch.arange(B, device="cuda") * 977 + 11) % cfg.vocab
+    ref = D.LlamaTP(cfg, batch=B, max_ctx=ctx + 1, seed=5, device="cuda", backend=OracleBackend)
+    t_ref = ref.step(tok, ctx)
+    l_ref = ref.last_logits.double()
+    del ref
+    torch.cuda.empty_cache()
+    gpu = D.LlamaTP(cfg, batch=B, max_ctx=ctx + 1, seed=5, device="cuda")
+    t_gpu = gpu.step(tok, ctx)
+    l_gpu = gpu.last_logits.double()
+    assert (l_gpu - l_ref).abs().max() / (1 + l_ref.abs().max()) < 2e-3
+    assert (t_gpu == t_ref).float().mean().item() >= 0.99 if B > 1 else torch.equal(t_gpu, t_ref)
 
 
 @pytest.mark.gpu

@@ -98,21 +98,27 @@ def test_pack_unpack_inverse_random(q, bits):
     assert np.array_equal(q.unpack_words(w, bits).cpu().numpy(), codes)
 
 
-def test_quantize_bit_exact_large(q):
-    """BASELINE shapes: 4096x11008 and 11008x4096 at every (b, g)."""
-    rng = np.random.default_rng(7)
-    for (K, N) in [(4096, 4096), (11008, 4096)]:
-        w = rng.normal(0, 0.02, (K, N)).astype(np.float32)
-        for bits in (2, 3, 4):
-            for g in (32, 64, 128, None):
-                cm = q.quantize_matrix(w, q.QuantConfig(bits, g))
-                codes, s, z = cm.numpy()
-                rc, rs, rz = orc.quantize_matrix(w, bits, g)
-                assert np.array_equal(codes, rc), (K, N, bits, g)
-                assert bits_equal(s, rs) and bits_equal(z, rz), (K, N, bits, g)
-                rowseq = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N)),
-                                          q.Layout.ROW_SEQUENTIAL).words.cpu().numpy()
-                assert np.array_equal(rowseq, orc.pack_rowseq(rc, bits)), (K, N, bits, g)
+@pytest.mark.parametrize("shape", [(4096, 4096), (4096, 11008), (11008, 4096)])
+def test_quantize_bit_exact_large(q, shape):
+    """BASELINE configs[1] shapes (4096^2, 4096x11008, 11008x4096) at every
+    (b, g): codes, scales, zeros, ROW_SEQUENTIAL and ZCURVE words bit-exact
+    against the oracle."""
+    K, N = shape
+    rng = np.random.default_rng(7 + K + 3 * N)
+    w = rng.normal(0, 0.02, (K, N)).astype(np.float32)
+    for bits in (2, 3, 4):
+        for g in (32, 64, 128, None):
+            cm = q.quantize_matrix(w, q.QuantConfig(bits, g))
+            codes, s, z = cm.numpy()
+            rc, rs, rz = orc.quantize_matrix(w, bits, g)
+            assert np.array_equal(codes, rc), (K, N, bits, g)
+            assert bits_equal(s, rs) and bits_equal(z, rz), (K, N, bits, g)
+            p = q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N))
+            rowseq = q.lay_out_blocks(cm, p, q.Layout.ROW_SEQUENTIAL).words.cpu().numpy()
+            assert np.array_equal(rowseq, orc.pack_rowseq(rc, bits)), (K, N, bits, g)
+            zc = q.lay_out_blocks(cm, p, q.Layout.ZCURVE).words.cpu().numpy()
+            assert np.array_equal(zc, orc.lay_out_words(rc, bits, p.m_b, p.t_b, True)), \
+                (K, N, bits, g)
 
 
 # --- panel layout ---------------------------------------------------------------
@@ -198,12 +204,8 @@ def test_qgemv_small_batch(q, tokens):
     cm, codes, s, z, rng = _case(q, K, N, 4, 64, seed=tokens)
     pw = q.PanelWeights.from_codes(cm)
     X = rng.normal(0, 1, (tokens, K)).astype(np.float32)
-    from paper_2307_03738_b200 import runtime as R
-    R.TC_ENABLED[0] = False  # the exact IMMA path at every token count
-    try:
-        Y = pw.gemv(torch.from_numpy(X).cuda()).cpu().numpy()
-    finally:
-        R.TC_ENABLED[0] = True
+    # the exact IMMA path at every token count
+    Y = pw.gemv(torch.from_numpy(X).cuda(), path="gemv").cpu().numpy()
     for t in range(tokens):
         yref = orc.qgemv_reference(codes, s, z, X[t])
         assert rel_err(Y[t], yref) <= TOL, (tokens, t)
@@ -343,7 +345,6 @@ TOL_TC = 2e-3  # tensor-core path: fp16 dequantized weights x fp16 activations, 
 def test_small_batch_tensor_core_path(q, tokens, g):
     """BASELINE configs[2] path (M >= 16): tcgen05 kernel vs the fp64 dense
     oracle (and vs the exact IMMA path), ragged N and token counts."""
-    from paper_2307_03738_b200 import runtime as R
     K, N = 2048, 1040
     cm, codes, s, z, rng = _case(q, K, N, 4, g, seed=tokens + g)
     pw = q.PanelWeights.from_codes(cm)
@@ -352,11 +353,7 @@ def test_small_batch_tensor_core_path(q, tokens, g):
     Y = pw.gemv(xt).cpu().numpy()
     ref = np.stack([orc.qgemv_reference(codes, s, z, X[t]) for t in range(tokens)])
     assert rel_err(Y, ref) <= TOL_TC
-    R.TC_ENABLED[0] = False
-    try:
-        Y2 = pw.gemv(xt).cpu().numpy()
-    finally:
-        R.TC_ENABLED[0] = True
+    Y2 = pw.gemv(xt, path="gemv").cpu().numpy()
     assert rel_err(Y2, ref) <= TOL
     # accumulate into y and fp16 activations
     Yacc = torch.from_numpy(Y).cuda()
@@ -368,17 +365,45 @@ def test_small_batch_tensor_core_path(q, tokens, g):
     assert rel_err(Yh, refh) <= TOL_TC
 
 
-def test_cfg2_shapes_tensor_core(q):
-    """configs[2]: K = N = 8192, 4-bit g64, M in {16, 64}."""
+@pytest.mark.parametrize("M", [1, 4, 16, 64])
+def test_cfg2_shapes_vs_oracle(q, M):
+    """configs[2]: K = N = 8192, 4-bit g64, M in {1, 4, 16, 64} against the CPU
+    oracle's dense fp64 product (oracle quantize, not the GPU's own dequantize).
+    The exact IMMA GEMV (SIMT path below 16 tokens) at 1e-5 for every M; the
+    tcgen05 path (auto from 16 tokens) at TOL_TC."""
     K = N = 8192
-    cm, codes, s, z, rng = _case(q, K, N, 4, 64, seed=99)
-    pw = q.PanelWeights.from_codes(cm)
-    wd = q.dequantize_matrix(cm).double()
-    for M in (16, 64):
-        X = torch.from_numpy(rng.normal(0, 1, (M, K)).astype(np.float32)).cuda()
-        Y = pw.gemv(X).double()
-        ref = X.double() @ wd
-        assert ((Y - ref).abs().max() / (1 + ref.abs().max())).item() <= TOL_TC
+    rng = np.random.default_rng(99 + M)
+    w = rng.normal(0, 0.02, (K, N)).astype(np.float32)
+    codes, s, z = orc.quantize_matrix(w, 4, 64)
+    cm = q.quantize_matrix(w, q.QuantConfig(4, 64))
+    pm = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N)))
+    X = rng.normal(0, 1, (M, K)).astype(np.float32)
+    ref = orc.qgemv_reference(codes, s, z, X)  # [M, N] fp64
+    Y = q.qgemv(pm, X)                          # the public seam, host in / host out
+    assert Y.shape == (M, N)
+    assert rel_err(Y, ref) <= (TOL if M < 16 else TOL_TC), M
+    pw = q.runtime.exec_layout(pm)
+    Yg = pw.gemv(torch.from_numpy(X).cuda(), path="gemv").cpu().numpy()
+    assert rel_err(Yg, ref) <= TOL, M
+
+
+@pytest.mark.parametrize("bits,g", [(4, 128), (3, 64), (2, 32), (4, None)])
+def test_qgemv_quantized_zero_mode(q, bits, g):
+    """ZeroMode.QUANTIZED (zeros rounded to codes, quant.py:88-90) through the
+    qgemv seam, the grouped launch and 2 tokens, vs the oracle."""
+    K, N = 4096, 1000
+    cm, codes, s, z, rng = _case(q, K, N, bits, g, seed=bits + (g or 0), zero_mode="quantized")
+    w = np.random.default_rng(bits + (g or 0)).normal(0, 0.02, (K, N)).astype(np.float32)
+    oc, os_, oz = orc.quantize_matrix(w, bits, g, "quantized")  # the same W as _case
+    assert np.array_equal(codes, oc) and bits_equal(s, os_) and bits_equal(z, oz)
+    assert np.all(z == np.round(z))  # integer zero points
+    pm = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N)))
+    X = rng.normal(0, 1, (2, K)).astype(np.float32)
+    ref = orc.qgemv_reference(codes, s, z, X)
+    assert rel_err(q.qgemv(pm, X[0]), ref[0]) <= TOL
+    assert rel_err(q.qgemv(pm, X), ref) <= TOL
+    (yb,) = q.qgemv_batch([pm], [X[1]])
+    assert rel_err(yb, ref[1]) <= TOL
 
 
 # --- grouped GEMV (independent GEMVs in one persistent launch) ----------------

@@ -16,7 +16,6 @@ ap.add_argument("--x-ready", type=int, default=0)
 ap.add_argument("--carveout", type=int, default=-1)
 args = ap.parse_args()
 L = _lib.lib()
-L.qigen_debug_carveout(args.carveout)
 dev = torch.device("cuda")
 for case in args.cases.split(","):
     shp, b, gs = case.split(":")

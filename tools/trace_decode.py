@@ -23,7 +23,6 @@ Lb = _lib.lib()
 import os
 Lb.qigen_debug_prefetch(int(os.environ.get('PRE', '-1')))
 Lb.qigen_debug_early_trigger(int(os.environ.get('EARLY', '0')))
-Lb.qigen_debug_carveout(int(os.environ.get('CARVE', '-1')))
 bufs = {}
 
 
