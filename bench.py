@@ -16,13 +16,19 @@ value  = algorithmic bytes (packed codes + f32 scale + f32 zero) of all ranks
          GEMV kernel over the 36 independent GEMVs (GemvGroup); inputs are
          resident in HBM.  config.chain_gbs reports the same GEMVs as 36
          dependent single-GEMV launches.
-e2e    = same metric through the public API `qgemv_batch(pms, xs_host)`: one
-         pinned H2D of all activations, the grouped launch, one D2H of all
-         outputs, every step.
-N > 1  = independent replicas of the sweep on every rank (weak scaling, no
-         data-path collective: GEMVs of distinct matrices are independent).
---impl reference = the reference's CPU path restated by the oracle (C port of
-         the generated kernel, oracle/qgemv_port.c, all host threads).
+e2e    = same metric through the public API `qgemv_batch(pms, xs_host)`: host
+         activations in, host results out, every step (zero-copy over PCIe).
+decode = BASELINE configs[3]/[4]: LLaMA-7B (B=1) and LLaMA-65B (B=1, B=8) decode
+         steps, tensor-parallel over the N ranks (NCCL), tokens/s and roofline.
+N > 1  = `--gpus N` re-executes itself under torch.distributed.run (one process
+         per GPU).  The sweep runs as independent replicas on every rank (weak
+         scaling, no data-path collective: GEMVs of distinct matrices are
+         independent); the decode steps are tensor-parallel across the ranks.
+cpu_baseline / --impl reference = the reference's CPU path on the box's host
+         cores: the C port of its generated kernel (oracle/qgemv_port.c, bit-
+         identical to the reference's numba kernel) on all 36 matrices at all
+         threads and at 1 thread, plus the reference's own numba kernel
+         (baseline/_ref, oracle/ref_numba.py) on configs[0].
 """
 
 from __future__ import annotations
@@ -150,45 +156,112 @@ class ClockSampler:
 # CPU side: the reference path restated by the oracle (C port, exec layout)
 # ---------------------------------------------------------------------------
 
-def build_cpu_cases(subset):
+def _cpu_case(args):
+    i, b, g, K, N = args
     from oracle import qigen_oracle as orc
-    cases = []
-    for i, (b, g, (K, N)) in enumerate(subset):
-        rng = np.random.default_rng(1000 + i)
-        w = rng.normal(0, 0.02, (K, N)).astype(np.float32)
-        codes, s, z = orc.quantize_matrix(w, b, g)
-        mu, tu, m_b, t_b = orc.plan(b, g, (K, N))
-        ex = orc.ExecLayout(orc.pack_rowseq(codes, b), s, z, K, N, b, g, m_b, t_b)
-        x = rng.normal(0, 1, K).astype(np.float32)
-        cases.append((ex, x, algo_bytes(K, N, b, g)))
-    return cases
+    rng = np.random.default_rng(1000 + i)
+    w = rng.normal(0, 0.02, (K, N)).astype(np.float32)
+    codes, s, z = orc.quantize_matrix(w, b, g)
+    mu, tu, m_b, t_b = orc.plan(b, g, (K, N))
+    ex = orc.ExecLayout(orc.pack_rowseq(codes, b), s, z, K, N, b, g, m_b, t_b)
+    x = rng.normal(0, 1, K).astype(np.float32)
+    return ex, x, algo_bytes(K, N, b, g), (b, g, K, N), (mu, tu, m_b, t_b)
+
+
+def build_cpu_cases(subset):
+    """Seeded sweep matrices quantized and laid out by the oracle's restatement
+    of the reference (quant.py / packing.py / Appendix B exec layout), built in
+    a process pool (untimed setup)."""
+    import multiprocessing as mp
+    jobs = [(i, b, g, K, N) for i, (b, g, (K, N)) in enumerate(subset)]
+    procs = max(1, min(len(jobs), len(os.sched_getaffinity(0)), 16))
+    if procs == 1:
+        return [_cpu_case(j) for j in jobs]
+    with mp.get_context("spawn").Pool(procs) as pool:
+        return pool.map(_cpu_case, jobs)
 
 
 def time_cpu(cases, reps, threads):
     from oracle import qigen_oracle as orc
-    for ex, x, _ in cases:  # warm-up (2 warm-ups)
+    for ex, x, *_ in cases:  # warm-up (SPEC.md:441: 2 warm-ups)
         orc.qgemv_port(ex, x, threads=threads)
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        for ex, x, _ in cases:
+        for ex, x, *_ in cases:
             orc.qgemv_port(ex, x, threads=threads)
         times.append(time.perf_counter() - t0)
     nbytes = sum(c[2] for c in cases)
     return nbytes / statistics.median(times) / 1e9, statistics.median(times)
 
 
-CPU_SAMPLE = [c for c in SWEEP if c[2] == (4096, 4096)]
+def cpu_threads() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+REF_NUMBA_CONFIGS = [(4, 128, (4096, 4096)), (2, 32, (4096, 4096))]  # configs[0] + a 2-bit one
+
+
+def time_ref_numba(cases, threads, reps=5):
+    """The reference's own numba-compiled kernel (oracle/ref_numba.py) on the
+    REF_NUMBA_CONFIGS matrices: compile (untimed), 2 warm-ups, median of reps,
+    at 1 thread and at `threads`.  None if the reference is not installed."""
+    from oracle import ref_numba
+    if ref_numba.available() is None:
+        return {"unavailable": "reference package not installed in baseline/_ref"}
+    out = {}
+    for c in cases:
+        ex, x, nbytes, (b, g, K, N), plan = c
+        if (b, g, (K, N)) not in REF_NUMBA_CONFIGS:
+            continue
+        t0 = time.perf_counter()
+        k = ref_numba.RefKernel(ex, b, g, plan)
+        k(x, 1)
+        compile_s = time.perf_counter() - t0
+        res = {"compile_s": round(compile_s, 1)}
+        for th in sorted({1, threads}):
+            for _ in range(2):
+                k(x, th)
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                k(x, th)
+                ts.append(time.perf_counter() - t0)
+            res[f"gbs_{th}t"] = round(nbytes / statistics.median(ts) / 1e9, 4)
+            res[f"ms_{th}t"] = round(1e3 * statistics.median(ts), 3)
+        out[f"b{b} g{g} {K}x{N}"] = res
+    return out
+
+
+def cpu_baseline_block(cases, steps_all=3, steps_one=1):
+    """cpu_baseline: the C port on all 36 matrices at all threads and at 1
+    thread, plus the reference's numba kernel on REF_NUMBA_CONFIGS."""
+    threads = cpu_threads()
+    gbs, t_all = time_cpu(cases, steps_all, threads)
+    gbs1, t_one = time_cpu(cases, steps_one, 1)
+    nbytes = sum(c[2] for c in cases)
+    return {
+        "value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+        "value_1thread": round(gbs1, 4),
+        "sample": (f"all {len(cases)} sweep matrices ({nbytes / 1e6:.0f} MB per pass; the GPU "
+                   f"arm's workload), C port of the reference's generated kernel "
+                   f"(oracle/qgemv_port.c, bit-identical to the reference's numba kernel) on its "
+                   f"exec layout; median of {steps_all} passes at {threads} threads "
+                   f"({1e3 * t_all:.1f} ms per pass), {steps_one} pass at 1 thread "
+                   f"({1e3 * t_one:.0f} ms)"),
+        "reference_numba": time_ref_numba(cases, threads),
+    }
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path on the host cores, same
+    workload (all 36 sweep matrices), metric and unit as our arm."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle import qigen_oracle as orc
-    threads = len(os.sched_getaffinity(0))
+    threads = cpu_threads()
     t0 = time.perf_counter()
-    cases = build_cpu_cases(CPU_SAMPLE)
+    cases = build_cpu_cases(SWEEP)
     setup = time.perf_counter() - t0
     for _ in range(args.warmup):
         time_cpu(cases, 1, threads)
@@ -198,20 +271,22 @@ def run_reference(args):
         times.append(t)
     nbytes = sum(c[2] for c in cases)
     value = nbytes * len(times) / sum(times) / 1e9
-    sample = (f"the 12 4096x4096 matrices of the sweep (b x g), {nbytes / 1e6:.1f} MB per step; "
-              f"C port of the reference's generated kernel on its exec layout, {threads} threads "
-              f"(setup {setup:.1f} s untimed)")
+    gbs1, t1 = time_cpu(cases, 1, 1)
+    sample = (f"all {len(cases)} sweep matrices (b x g x shape), {nbytes / 1e6:.1f} MB per step; "
+              f"C port of the reference's generated kernel (bit-identical to its numba kernel) "
+              f"on its exec layout, {threads} threads; 1 thread: {gbs1:.3f} GB/s "
+              f"({1e3 * t1:.0f} ms per step); setup {setup:.1f} s untimed")
     line = {"metric": "quantized GEMV effective HBM GB/s", "value": round(value, 4), "unit": "GB/s",
             "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample": "4096x4096 slice"},
+            "config": {"workload": WORKLOAD, "matrices": len(cases), "bytes_per_step": nbytes},
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "value_1thread": round(gbs1, 4), "sample": sample,
+                             "reference_numba": time_ref_numba(cases, threads)},
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-    _ = orc
     return 0
 
 
@@ -223,10 +298,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = init_dist()
     import paper_2307_03738_b200 as q
     from paper_2307_03738_b200.runtime import PanelWeights
 
@@ -317,7 +389,8 @@ def run_ours(args):
     chain_gbs = STEP_BYTES * chain_steps / (chain_ms / 1e3) / 1e9
 
     # --- e2e through the public API with host buffers --------------------------
-    # qgemv_batch(pms, xs): one H2D of all x, the grouped launch, one D2H of all y
+    # qgemv_batch(pms, xs): host x gathered into pinned memory, the grouped launch
+    # reads it and stores y into a fresh pinned block over PCIe (zero-copy), sync
     xs_host = [x.cpu().numpy() for x in xs]
     e2e_steps = max(1, min(args.steps, 200))
     for _ in range(max(3, args.warmup)):  # warm-up (plan, staging and pinned result blocks cached)
@@ -337,6 +410,18 @@ def run_ours(args):
     e2e = STEP_BYTES * world * e2e_steps / e2e_s / 1e9
     h2d = sum(K * 4 for _, _, (K, N) in SWEEP)
     d2h = sum(N * 4 for _, _, (K, N) in SWEEP)
+    del group, graph, chain_graph
+    torch.cuda.synchronize()
+
+    # --- decode steps (configs[3]/[4]), tensor parallel over the ranks ----------
+    decode = {}
+    if not args.no_decode:
+        dsteps = max(3, min(args.steps, 50))
+        for wl, B in DECODE_DEFAULT:
+            try:
+                decode[f"{wl} B={B}"] = measure_decode(wl, B, 0, 0, dsteps, args.warmup)
+            except Exception as e:  # noqa: BLE001 (reported in the line, not fatal)
+                decode[f"{wl} B={B}"] = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     if rank == 0:
         peak, peak_src = measured_peak()
@@ -363,15 +448,10 @@ def run_ours(args):
             "gpu_launches": k_ours * args.steps,
             "kernels_per_step": {"ours": k_ours, "all": k_total},
             "clocks": sampler.report(),
+            "decode": decode,
         }
         if not args.no_cpu_baseline:
-            threads = len(os.sched_getaffinity(0))
-            cases = build_cpu_cases(CPU_SAMPLE)
-            gbs, _ = time_cpu(cases, 3, threads)
-            line["cpu_baseline"] = {
-                "value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                "sample": "12 4096x4096 matrices of the sweep, median of 3 passes, C port of the "
-                          "reference's generated kernel (oracle/qgemv_port.c)"}
+            line["cpu_baseline"] = cpu_baseline_block(build_cpu_cases(SWEEP))
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -379,26 +459,24 @@ def run_ours(args):
     return 0
 
 
-def run_decode(args):
-    """BASELINE configs[3]/[4]: one decode step of a random-init LLaMA shard per
-    GPU (tensor parallel over the ranks), replayed as a CUDA graph."""
+def measure_decode(workload, B, ctx, layers, steps, warmup, tp_shard=0):
+    """One decode step of a random-init LLaMA shard per GPU (tensor parallel
+    over the ranks of the process group), replayed as a CUDA graph: device
+    tokens/s (max over ranks), roofline on bytes/step, e2e with token ids from
+    and to pinned host memory.  Returns a dict (identical on every rank)."""
     import torch
     import torch.distributed as dist
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2307_03738_b200 import decode as D
 
-    cfg = D.LLAMA_7B if args.workload == "llama7b" else D.LLAMA_65B
-    if args.layers:
-        cfg = D.shrink(cfg, n_layers=args.layers)
-    ctx = args.ctx or (512 if args.workload == "llama7b" else 1024)
-    B = args.batch
+    rank, world, local = dist_env()
+    cfg = D.LLAMA_7B if workload == "llama7b" else D.LLAMA_65B
+    if layers:
+        cfg = D.shrink(cfg, n_layers=layers)
+    ctx = ctx or (512 if workload == "llama7b" else 1024)
     t0 = time.perf_counter()
-    tp = D.ShardTP(args.tp_shard) if args.tp_shard > 1 else D.TP()
+    tp = D.ShardTP(tp_shard) if tp_shard > 1 else D.TP()
     model = D.LlamaTP(cfg, batch=B, max_ctx=ctx + 1, seed=0, tp=tp)
+    torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     tok = torch.zeros(B, dtype=torch.long, device="cuda")
     pos = ctx  # ctx past tokens in the cache, this step writes position ctx
@@ -420,14 +498,14 @@ def run_decode(args):
             k_total = k_ours = None
         sampler = ClockSampler(local)
         with sampler:
-            for _ in range(args.warmup):
+            for _ in range(warmup):
                 graph.replay()
             stream.synchronize()
             if world > 1:
                 dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for _ in range(args.steps):
+            for _ in range(steps):
                 graph.replay()
             e1.record(stream)
             e1.synchronize()
@@ -436,14 +514,14 @@ def run_decode(args):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    ms_step = ms / args.steps
+    ms_step = ms / steps
     # e2e: token ids in from pinned host memory, next ids back, every step
     tok_h = torch.zeros(B, dtype=torch.long).pin_memory()
     out_h = torch.zeros(B, dtype=torch.long).pin_memory()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    n_e2e = min(args.steps, 50)
+    n_e2e = min(steps, 50)
     w0 = time.perf_counter()
     with torch.cuda.stream(stream):
         for _ in range(n_e2e):
@@ -461,31 +539,57 @@ def run_decode(args):
         t = torch.tensor([float(nbytes)], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         nbytes = int(t.item())
+    peak, peak_src = measured_peak()
+    gbs = nbytes / (ms_step / 1e3) / 1e9
+    comm = getattr(model, "comm_kind", None)
+    res = {
+        "value": round(B / (ms_step / 1e3), 2), "unit": "tokens/s",
+        "ms_per_step": round(ms_step, 4), "steps": steps,
+        "config": {"workload": f"{workload} decode step", "layers": cfg.n_layers,
+                   "d_model": cfg.d_model, "bits": cfg.bits, "group": cfg.group, "batch": B,
+                   "ctx": ctx, "setup_s": round(setup_s, 1),
+                   "parallelism": (f"tp{tp_shard} shard of rank 0 on one GPU, collectives "
+                                   f"skipped (per-GPU compute only)") if tp_shard > 1
+                   else f"tp{world}", "allreduce": comm},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": round(gbs / peak, 4),
+                     "bytes_per_step_per_gpu": nbytes, "traffic": None},
+        "e2e": {"value": round(B / e2e_s, 2), "unit": "tokens/s", "h2d_bytes_per_step": 8 * B,
+                "d2h_bytes_per_step": 8 * B},
+        "gpu_launches": None if k_ours is None else k_ours * steps,
+        "kernels_per_step": {"ours": k_ours, "all": k_total},
+        "clocks": sampler.report(),
+    }
+    del graph, model
+    torch.cuda.empty_cache()
+    return res
+
+
+def init_dist():
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show the N ranks
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def run_decode(args):
+    """BASELINE configs[3]/[4] as the line's own metric (--workload)."""
+    import torch.distributed as dist
+    rank, world, local = init_dist()
+    r = measure_decode(args.workload, args.batch, args.ctx, args.layers, args.steps,
+                       args.warmup, args.tp_shard)
     if rank == 0:
-        peak, peak_src = measured_peak()
-        gbs = nbytes / (ms_step / 1e3) / 1e9
-        line = {
-            "metric": "decode tokens/s", "value": round(B / (ms_step / 1e3), 2), "unit": "tokens/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u8 x s8 -> s32 (IMMA) linears, f16 KV/lm_head",
-            "data": "synthetic (random-init weights, random fp16 KV cache)",
-            "config": {"workload": f"{args.workload} decode step", "layers": cfg.n_layers,
-                       "d_model": cfg.d_model, "bits": cfg.bits, "group": cfg.group,
-                       "batch": B, "ctx": ctx,
-                       "parallelism": (f"tp{args.tp_shard} shard of rank 0 on one GPU, collectives "
-                                       f"skipped (per-GPU compute only)") if args.tp_shard > 1
-                       else f"tp{world}",
-                       "setup_s": round(setup_s, 1)},
-            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
-                         "peak_source": peak_src, "unit": "GB/s", "frac": round(gbs / peak, 4),
-                         "bytes_per_step_per_gpu": nbytes, "traffic": None},
-            "e2e": {"value": round(B / e2e_s, 2), "unit": "tokens/s", "h2d_bytes_per_step": 8 * B,
-                    "d2h_bytes_per_step": 8 * B},
-            "gpu_launches": None if k_ours is None else k_ours * args.steps,
-            "kernels_per_step": {"ours": k_ours, "all": k_total},
-            "clocks": sampler.report(),
-        }
+        line = {"metric": "decode tokens/s", "value": r["value"], "unit": "tokens/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u8 x s8 -> s32 (IMMA) linears, f16 KV/lm_head",
+                "data": "synthetic (random-init weights, random fp16 KV cache)"}
+        line.update({k: r[k] for k in ("config", "roofline", "e2e", "gpu_launches",
+                                        "kernels_per_step", "clocks")})
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -493,15 +597,45 @@ def run_decode(args):
     return 0
 
 
+DECODE_DEFAULT = [("llama7b", 1), ("llama65b", 1), ("llama65b", 8)]
+
+
+def _kernel_sources_sha16() -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for name in ("gemv_grouped.cu", "gemv_common.cuh", "common.cuh"):
+        h.update((ROOT / "paper_2307_03738_b200" / "csrc" / name).read_bytes())
+    return h.hexdigest()[:16]
+
+
 def _traffic():
-    """DRAM bytes per step from the committed ncu summary, if one exists."""
+    """DRAM bytes per step from the committed ncu capture, only if it was taken
+    on the current kernel sources (profiles/traffic.json records their hash);
+    otherwise None (never a stale number)."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         try:
-            return json.loads(p.read_text()).get("dram_bytes_per_step")
+            d = json.loads(p.read_text())
+            if d.get("kernel_sources_sha16") == _kernel_sources_sha16():
+                return d.get("dram_bytes_per_step")
         except Exception:  # noqa: BLE001
             return None
     return None
+
+
+def relaunch_distributed(n: int) -> int:
+    """`--gpus N` outside torchrun: re-execute under torch.distributed.run, one
+    process per GPU (127.0.0.1 rendezvous)."""
+    import socket
+    import subprocess
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -511,6 +645,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decode", action="store_true",
+                    help="skip the decode measurements (configs[3]/[4]) of the default line")
     ap.add_argument("--workload", choices=["sweep", "llama7b", "llama65b"], default="sweep")
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--ctx", type=int, default=0)
@@ -521,6 +657,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload != "sweep":
