@@ -261,7 +261,8 @@ struct SmemLayout {
   __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int TP, int M, int WPC,
                                  int S) {
     stage = bits * 512 + szb;
-    const int max_units = max_steps;  // units are >= 32 rows
+    // units are >= 32 rows, except g = 16 (szb 2048: 16 groups per superstep)
+    const int max_units = szb == 16 * 128 ? 2 * max_steps : max_steps;
     int off = 0;
     ring = off;  off += WPC * D * stage;
     bars = off;  off += WPC * D * 8;
@@ -277,12 +278,15 @@ struct SmemLayout {
   }
 };
 
-// GPS = quantisation groups closed per superstep: 8, 4, 2, 1 for g = 32, 64,
-// 128, 256 (their (s, z) ride in the stage), 0 for longer groups (g a multiple
-// of 256 or full column; (s, z) prefetched from global one group ahead).
-// Exponent/flush unit U = min(g, 128) rows: the activations of one unit share a
-// fixed-point exponent (found with one REDUX, no CTA barrier), and the integer
-// accumulators are folded into f32 once per unit.
+// GPS = quantisation groups closed per superstep: 16, 8, 4, 2, 1 for g = 16,
+// 32, 64, 128, 256 (their (s, z) ride in the stage), 0 for longer groups (g a
+// multiple of 256 or full column; (s, z) prefetched from global one group
+// ahead).  Exponent/flush unit U = min(g, 128) rows: the activations of one unit
+// share a fixed-point exponent (found with one REDUX, no CTA barrier), and the
+// integer accumulators are folded into f32 once per unit.  g = 16 (
+// the reference unrolls groups inside a packing unit, kernelgen.py:289-310): a
+// group is half an m16n8k32 step, so each step issues two m16n8k16 IMMAs (the
+// A fragment's k halves, the B digit words' halves) and flushes after each.
 template <int BITS, int NB, int WPC, int GPS>
 __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -290,8 +294,8 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   constexpr int TP = 2 * NB;                // tokens in the fragment layout (padded)
   constexpr int SZB = GPS * 128;
   constexpr int UPS = GPS > 2 ? GPS : 2;   // flush units per superstep
-  constexpr int SPU = 8 / UPS;             // steps per unit
-  constexpr int IPU = SPU * 8;             // prologue items (4 rows) per unit
+  constexpr int SPU = GPS == 16 ? 1 : 8 / UPS;  // steps per unit (g = 16: half a step)
+  constexpr int IPU = GPS == 16 ? 4 : SPU * 8;  // prologue items (4 rows) per unit
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t = lane & 3;
   const int S = gridDim.y, ys = blockIdx.y;
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   const bool xon = (t & 1) == 0;  // lanes holding digits (d0, d1) carry the z X term
   const int tcol = t >> 1;        // token offset of this lane's accumulator columns
   const float2* szg = (const float2*)zsrc;
-  const int spg = a.g ? a.g / kStep : a.KS * 8;  // steps per group
+  const int spg = GPS == 0 ? (a.g ? a.g / kStep : a.KS * 8) : 1;  // steps per (long) group
   int gcur = ks0 * 8 / spg;
   float2 szr0 = make_float2(0.f, 0.f), szr1 = szr0;
   if (GPS == 0) {
@@ -520,20 +524,44 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     for (int sl = 0; sl < 8; ++sl) {
       uint32_t af[4];
       extract<BITS>(w, sl, af);
+      if constexpr (GPS == 16) {
+        // two groups per step: k16 IMMA on each half, flush each
+        constexpr int sh = BITS == 2 ? 4 : 0;  // 2-bit odd steps carry an extra x16
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) imma(acc[sl % AC][nb], af, bs[(sl * TP + 2 * nb) * 16]);
-      constexpr int SPG = GPS > 0 ? 8 / GPS : 8;  // steps per group (short groups)
-      if ((sl + 1) % SPU == 0) {
-        const int uj = (sl + 1) / SPU - 1;  // unit within the superstep
-        const int u = s * UPS + uj;
-        if (GPS > 0) {
-          const int gi = GPS >= UPS ? uj : 0;  // g = 256: both units use group 0
-          flush(u, szs[gi * 16 + gq], szs[gi * 16 + gq + 8]);
-        } else {
-          flush(u, szr0, szr1);
+        for (int h = 0; h < 2; ++h) {
+          int c16[NB][4];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const uint2 b = bs[(sl * TP + 2 * nb) * 16];
+            imma16(c16[nb], af[2 * h], af[2 * h + 1], h ? b.y : b.x);
+          }
+          const int u = s * 16 + 2 * sl + h;
+          const float2 sz0 = szs[(2 * sl + h) * 16 + gq], sz1 = szs[(2 * sl + h) * 16 + gq + 8];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const float2 xv = xs[u * TP + 2 * nb + tcol];
+            const float X = xon ? xv.x : 0.f, sc = xv.y;
+            const int k = (sl & 1) ? sh : 0;
+            const float q0 = (float)((c16[nb][0] >> k) * 256 + (c16[nb][1] >> k));
+            const float q1 = (float)((c16[nb][2] >> k) * 256 + (c16[nb][3] >> k));
+            yv[nb][0] = fmaf(sz0.x * sc, fmaf(-sz0.y, X, q0 * w_lo), yv[nb][0]);
+            yv[nb][1] = fmaf(sz1.x * sc, fmaf(-sz1.y, X, q1 * w_hi), yv[nb][1]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) imma(acc[sl % AC][nb], af, bs[(sl * TP + 2 * nb) * 16]);
+        if ((sl + 1) % SPU == 0) {
+          const int uj = (sl + 1) / SPU - 1;  // unit within the superstep
+          const int u = s * UPS + uj;
+          if (GPS > 0) {
+            const int gi = GPS >= UPS ? uj : 0;  // g = 256: both units use group 0
+            flush(u, szs[gi * 16 + gq], szs[gi * 16 + gq + 8]);
+          } else {
+            flush(u, szr0, szr1);
+          }
         }
       }
-      (void)SPG;
     }
     if (GPS == 0 && ((ks0 + s + 1) * 8) % spg == 0) {  // long group closed
       ++gcur;
@@ -672,7 +700,7 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   auto kern = gemv_kernel<BITS, NB, WPC, GPS>;
   constexpr int TP = 2 * NB;
   constexpr int UPS = GPS > 2 ? GPS : 2;
-  constexpr int IPU = (8 / UPS) * 8;
+  constexpr int IPU = GPS == 16 ? 4 : (8 / UPS) * 8;
   static OncePerDevice once;
   const int cst = once.run([&]() -> int {
     QIGEN_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -831,6 +859,7 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
 template <int BITS, int NB, int WPC>
 static int launch_gps(GemvArgs& a, int S, cudaStream_t stream) {
   switch (a.g) {
+    case 16: return launch_cfg<BITS, NB, WPC, 16>(a, S, stream);
     case 32: return launch_cfg<BITS, NB, WPC, 8>(a, S, stream);
     case 64: return launch_cfg<BITS, NB, WPC, 4>(a, S, stream);
     case 128: return launch_cfg<BITS, NB, WPC, 2>(a, S, stream);
@@ -900,7 +929,7 @@ extern "C" int qigen_debug_force_prep(int on) {
 }
 extern "C" int64_t qigen_gemv_workspace_size(int64_t n, int64_t tokens) {
   const int64_t tp = tokens <= 2 ? 2 : tokens <= 4 ? 4 : tokens <= 8 ? 8 : 16;
-  return supersteps(n) * 8 * tp * (128 + 8);
+  return supersteps(n) * 8 * tp * (128 + 16);  // digits + unit factors (g = 16: 2 units per step)
 }
 
 extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
@@ -914,9 +943,10 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   QIGEN_CHECK_ARG(n > 0 && m > 0, QIGEN_ERR_ARG, "empty matrix");
   QIGEN_CHECK_ARG(group == 0 || (n % group == 0), QIGEN_ERR_CONFIG,
                   "group size %lld does not divide row count %lld", (long long)group, (long long)n);
-  QIGEN_CHECK_ARG(group == 0 || group == 32 || group == 64 || group == 128 || group % kSuper == 0,
+  QIGEN_CHECK_ARG(group == 0 || group == 16 || group == 32 || group == 64 || group == 128 ||
+                      group % kSuper == 0,
                   QIGEN_ERR_UNSUPPORTED,
-                  "group size %lld: the GEMV takes 32, 64, 128 or a multiple of 256 (or full "
+                  "group size %lld: the GEMV takes 16, 32, 64, 128 or a multiple of 256 (or full "
                   "column)", (long long)group);
   QIGEN_CHECK_ARG(tokens >= 1 && tokens <= 16, QIGEN_ERR_UNSUPPORTED,
                   "the GEMV path takes 1..16 activation rows, got %lld", (long long)tokens);

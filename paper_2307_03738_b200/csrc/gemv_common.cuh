@@ -75,6 +75,16 @@ __device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint2 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
 }
 
+// m16n8k16 IMMA (zero accumulator input): A = one k half of the k32 fragment
+// (a0: rows gq, a1: rows gq+8), B = the matching digit word.
+__device__ __forceinline__ void imma16(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%7,%7,%7,%7};"
+      : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
+      : "r"(a0), "r"(a1), "r"(b), "r"(0));
+}
+
 // Fragment registers of local step sl (0..7) from the lane's superstep words.
 // Codes stay in place (one AND each); every accumulator row then carries a
 // power-of-two scale: RowScale<BITS>::hi for rows gq+8 (rows gq: 1), and for

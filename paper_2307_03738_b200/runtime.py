@@ -267,6 +267,12 @@ class GemvGroup:
         self._h = h
         self.nbytes_algorithmic = sum(pw.nbytes_algorithmic() for pw, _, _ in entries)
 
+    @staticmethod
+    def supports(pw: "PanelWeights") -> bool:
+        """The grouped kernel's configurations: every group size the GEMV takes
+        except g = 16 (whose per-half-step flush the grouped records do not carry)."""
+        return pw.config.group_size != 16
+
     def run(self) -> None:
         call("qigen_gemv_group_run", self._h, _dev.stream_handle())
 
@@ -359,15 +365,30 @@ class _Batch:
         # counter are per list: concurrent calls on one list take turns
         self.lock = threading.Lock()
         self.done = None  # event after the last device-path call (other streams wait on it)
+        # matrices the grouped kernel takes, and the rest (g = 16: a flush every
+        # half step; run as single GEMVs right after the grouped launch)
+        self.gi = [i for i, pw in enumerate(self.pws) if GemvGroup.supports(pw)]
+        self.si = [i for i in range(len(self.pws)) if i not in set(self.gi)]
+
+    def _xs(self, buf, i):
+        return buf[self.koff[i]:self.koff[i + 1]]
+
+    def _ys(self, buf, i):
+        return buf[self.noff[i]:self.noff[i + 1]]
 
     @property
-    def group(self) -> "GemvGroup":
+    def group(self) -> "GemvGroup | None":
         """Grouped launch over device inputs (``x``), built on first use."""
-        if self._group is None:
-            self._group = GemvGroup([(pw, self.x[self.koff[i]:self.koff[i + 1]],
-                                      self.y[self.noff[i]:self.noff[i + 1]])
-                                     for i, pw in enumerate(self.pws)])
+        if self._group is None and self.gi:
+            self._group = GemvGroup([(self.pws[i], self._xs(self.x, i), self._ys(self.y, i))
+                                     for i in self.gi])
         return self._group
+
+    def run_device(self) -> None:
+        if self.group is not None:
+            self.group.run()
+        for i in self.si:
+            self.pws[i].gemv(self._xs(self.x, i), out=self._ys(self.y, i))
 
     @property
     def group_host(self) -> "GemvGroup":
@@ -379,9 +400,9 @@ class _Batch:
             # onto a fresh pinned block (qigen_gemv_group_run_rebased)
             self.yh0 = torch.empty(self.y.numel(), pin_memory=True)
             self.yh0_ptr = self.yh0.data_ptr()
-            self._group_host = GemvGroup([(pw, self.xh[self.koff[i]:self.koff[i + 1]],
-                                           self.yh0[self.noff[i]:self.noff[i + 1]])
-                                          for i, pw in enumerate(self.pws)], pinned_x=True)
+            self._group_host = GemvGroup([(self.pws[i], self._xs(self.xh, i),
+                                           self._ys(self.yh0, i)) for i in self.gi],
+                                         pinned_x=True) if self.gi else None
         return self._group_host
 
 
@@ -393,7 +414,13 @@ def _batch_host_run(b: "_Batch"):
     # no cudaHostAlloc after warm-up) that the returned views own, so no
     # host-side copy out of a shared staging buffer is needed.
     yh = torch.empty(b.y.numel(), pin_memory=True)
-    call("qigen_gemv_group_run_rebased", gh._h, b.yh0_ptr, yh.data_ptr(), _dev.stream_handle())
+    if gh is not None:
+        call("qigen_gemv_group_run_rebased", gh._h, b.yh0_ptr, yh.data_ptr(),
+             _dev.stream_handle())
+    for i in b.si:  # matrices outside the grouped kernel: single GEMVs, staged copies
+        xd = b._xs(b.x, i)
+        xd.copy_(b._xs(b.xh, i), non_blocking=True)
+        b._ys(yh, i).copy_(b.pws[i].gemv(xd), non_blocking=True)
     torch.cuda.current_stream().synchronize()
     yv = yh.numpy()
     return [yv[s] for s in b.yslices]
@@ -474,7 +501,7 @@ def _batch_call(b: "_Batch", xs):
     if b.done is not None:
         cur.wait_event(b.done)
     torch.cat([x.reshape(-1).float() for x in xs], out=b.x)
-    b.group.run()
+    b.run_device()
     out = list(torch.split(b.y.clone(), [pw.m for pw in b.pws]))
     b.done = torch.cuda.Event()
     b.done.record(cur)

@@ -155,9 +155,8 @@ def _case(q, K, N, bits, g, seed=0, zero_mode="real32"):
 def test_qgemv_vs_reference_kernel_golden(q, golden_qgemv):
     """Against the outputs of the reference's own generated kernels."""
     data, cases = golden_qgemv
-    for c in cases:
-        if c["g"] is not None and c["g"] % 32:
-            continue  # g=16 is outside the GEMV path (see DESIGN.md)
+    assert any(c["g"] == 16 for c in cases)
+    for c in cases:  # every fixture, g = 16 included
         k = c["key"]
         cfg = q.QuantConfig(c["bits"], c["g"])
         cm = q.quantize_matrix(data[k + "_w"], cfg)
@@ -236,6 +235,91 @@ def test_qgemv_ragged_shapes(q, shape, bits):
         pm = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N)))
         x = rng.normal(0, 1, K).astype(np.float32)
         assert rel_err(q.qgemv(pm, x), orc.qgemv_reference(codes, s, z, x)) <= TOL
+
+
+def test_acceptance_1_oracle_equivalence(q):
+    """SPEC acceptance #1: every bits in {2,3,4} x grouping in
+    {16, 32, 64, 128, FULL_COLUMN} on 20 random shapes with n, m <= 1024: qgemv
+    matches qgemv_reference within relative max-norm 1e-5."""
+    rng = np.random.default_rng(454)
+    for bits in (2, 3, 4):
+        unit = q.pack_unit(bits)[0]
+        for g in (16, 32, 64, 128, None):
+            step = unit if g is None else int(np.lcm(unit, g))
+            for _ in range(20):
+                K = int(rng.integers(1, 1024 // step + 1)) * step
+                N = int(rng.integers(1, 1025))
+                w = rng.normal(0, 0.02, (K, N)).astype(np.float32)
+                codes, s, z = orc.quantize_matrix(w, bits, g)
+                cm = q.quantize_matrix(w, q.QuantConfig(bits, g))
+                pm = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N)))
+                x = rng.normal(0, 1, K).astype(np.float32)
+                err = rel_err(q.qgemv(pm, x), orc.qgemv_reference(codes, s, z, x))
+                assert err <= TOL, (bits, g, K, N, err)
+
+
+def test_acceptance_6_thread_invariance(q):
+    """SPEC acceptance #6: qgemv output bit-identical for threads = 1, 2, 4, 8
+    (`threads` has no GPU meaning; the kernel's reduction order is fixed)."""
+    rng = np.random.default_rng(6)
+    for K, N, bits, g in [(1024, 1000, 4, 64), (768, 333, 3, None), (512, 64, 2, 16)]:
+        cm = q.quantize_matrix(rng.normal(0, 0.02, (K, N)).astype(np.float32),
+                               q.QuantConfig(bits, g))
+        pm = q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N)))
+        x = rng.normal(0, 1, K).astype(np.float32)
+        ys = [q.qgemv(pm, x, threads=t) for t in (1, 2, 4, 8)]
+        assert all(np.array_equal(ys[0], y) for y in ys[1:])
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+@pytest.mark.parametrize("shape", [(4096, 4096), (4096, 11008), (11008, 4096), (352, 1000)])
+def test_qgemv_group16(q, bits, shape):
+    """g = 16 (two groups per m16n8k32 step: k16 IMMAs, a flush per half step)
+    at BASELINE shapes and a ragged one: 1 / 3 / 8 tokens, the forced prep-kernel
+    path and the RMSNorm prologue, against the oracle."""
+    from paper_2307_03738_b200 import _lib
+    K, N = shape
+    if K % q.pack_unit(bits)[0]:
+        pytest.skip("K must fill packing units")
+    cm, codes, s, z, rng = _case(q, K, N, bits, 16, seed=K + bits)
+    pw = q.PanelWeights.from_codes(cm)
+    for tokens in (1, 3, 8):
+        X = rng.normal(0, 1, (tokens, K)).astype(np.float32)
+        ref = orc.qgemv_reference(codes, s, z, X)
+        Y = pw.gemv(torch.from_numpy(X).cuda()).cpu().numpy()
+        assert rel_err(Y, ref) <= TOL, (tokens, rel_err(Y, ref))
+    try:
+        _lib.lib().qigen_debug_force_prep(1)
+        Yp = pw.gemv(torch.from_numpy(X).cuda()).cpu().numpy()
+    finally:
+        _lib.lib().qigen_debug_force_prep(0)
+    assert rel_err(Yp, ref) <= TOL
+    wn = rng.uniform(0.5, 1.5, K).astype(np.float32)
+    Yn = pw.gemv(torch.from_numpy(X).cuda(), prologue="rmsnorm",
+                 norm_weight=torch.from_numpy(wn).cuda()).cpu().numpy()
+    for t in range(tokens):
+        xn = X[t] / np.sqrt(np.mean(X[t].astype(np.float64) ** 2) + 1e-5) * wn
+        assert rel_err(Yn[t], orc.qgemv_reference(codes, s, z, xn)) <= TOL
+
+
+def test_qgemv_batch_with_group16(q):
+    """qgemv_batch over a list mixing g = 16 (single GEMVs after the grouped
+    launch) with grouped-kernel configs, host and device inputs."""
+    pms, xs, refs = [], [], []
+    for i, (K, N, b, g) in enumerate([(1024, 512, 4, 16), (2048, 300, 3, 32), (512, 100, 2, 16),
+                                      (768, 640, 4, None)]):
+        cm, codes, s, z, rng = _case(q, K, N, b, g, seed=90 + i)
+        pms.append(q.lay_out_blocks(cm, q.plan(q.DEFAULT_HARDWARE, cm.config, (K, N))))
+        xs.append(rng.normal(0, 1, K).astype(np.float32))
+        refs.append(orc.qgemv_reference(codes, s, z, xs[-1]))
+    for _ in range(2):
+        for y, r in zip(q.qgemv_batch(pms, xs), refs):
+            assert rel_err(y, r) <= TOL
+    for y, r in zip(q.qgemv_batch(pms, [torch.from_numpy(x).cuda() for x in xs]), refs):
+        assert rel_err(y.cpu().numpy(), r) <= TOL
+    only16 = [pms[0], pms[2]]
+    for y, r in zip(q.qgemv_batch(only16, [xs[0], xs[2]]), [refs[0], refs[2]]):
+        assert rel_err(y, r) <= TOL
 
 
 def test_qgemv_properties(q):
@@ -549,6 +633,7 @@ def test_group_gemv_run_rebased(q):
 
 
 def test_group_gemv_rejects_bad_input(q):
+    """The grouped kernel does not take g = 16 (qgemv_batch routes it to single GEMVs)."""
     from paper_2307_03738_b200.runtime import GemvGroup
     cm, *_ = _case(q, 512, 64, 4, 16)
     pw = q.PanelWeights.from_codes(cm)
