@@ -217,6 +217,64 @@ int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads, int64_t he
                       int64_t ctx, int64_t pos, float scale, float* out, void* workspace,
                       int64_t workspace_bytes, void* stream);
 
+/* ---- tensor-parallel one-shot all-reduce (decode driver)
+ * Row-parallel layers push their partial outputs from the GEMV epilogue
+ * straight into every rank's inbox over NVLink (peer-mapped device memory) and
+ * count the columns they delivered; each rank then adds the partials to its
+ * residual in rank order.  No NCCL call on the data path; results bit-identical
+ * on every rank.  Protocol and layout: csrc/tp.cuh, DESIGN.md §7.  Replaces the
+ * torch.distributed/NCCL all-reduce the driver issues after o_proj and
+ * down_proj (no reference counterpart: the reference is single-process,
+ * SPEC.md:376). */
+typedef struct qigen_tp_comm qigen_tp_comm;
+/* Bytes of each rank's buffer (header + 2 slots x world x max_tokens x d f32). */
+int64_t qigen_tp_buffer_size(int world, int64_t d, int64_t max_tokens);
+/* cudaMalloc + zero a buffer; ipc_handle_out (64 bytes, or NULL) receives its
+ * cudaIpcMemHandle for the peers. */
+int qigen_tp_alloc(int64_t bytes, void** ptr, void* ipc_handle_out);
+int qigen_tp_free(void* ptr);
+/* Map a peer's buffer (cudaIpcOpenMemHandle, lazy peer access). */
+int qigen_tp_open_peer(const void* ipc_handle, void** ptr);
+int qigen_tp_close_peer(void* ptr);
+/* bases[q] = rank q's buffer as addressable from this process (bases[rank] is
+ * this rank's own).  Ranks emulated on one GPU pass each other's plain device
+ * pointers.  `layers` = uses of each slot per decode step. */
+int qigen_tp_create(int rank, int world, int64_t d, int64_t max_tokens, int layers,
+                    void* const* bases, qigen_tp_comm** out);
+int qigen_tp_destroy(qigen_tp_comm* comm);
+/* Start of a decode step on this rank (advances the epoch the reduces wait for). */
+int qigen_tp_step_begin(const qigen_tp_comm* comm, void* stream);
+/* Row-parallel qigen_gemv_ex (accumulate 0, automatic K split) whose epilogue
+ * stores the partial into slot `slot` of every rank instead of a local y. */
+int qigen_gemv_tp_push(const qigen_tp_comm* comm, int slot, const uint32_t* qw, const float* qsz,
+                       int64_t n, int64_t m, int bits, int64_t group_size, const void* x,
+                       int x_dtype, int64_t tokens, int64_t ldx, int prologue,
+                       const float* prologue_w, float eps, void* workspace,
+                       int64_t workspace_bytes, void* stream);
+/* h[tokens, d] += sum of the ranks' partials of slot `slot`, use `layer` of the
+ * current step, in rank order (waits for every rank's columns; a wait longer
+ * than 4 s sets the error flag instead of hanging). */
+int qigen_tp_reduce(const qigen_tp_comm* comm, int slot, int layer, float* h, int64_t tokens,
+                    void* stream);
+/* 1 if a reduce on this rank timed out since the last call (then cleared). */
+int qigen_tp_error(const qigen_tp_comm* comm, int* out);
+
+/* Vocab-parallel LM head with the greedy argmax fused: for each
+ * of `batch` (1..8) tokens, xn = fp16(h * rsqrt(mean(h^2) + eps) * norm_w),
+ * logits[b, v] = xn . W[v] (W fp16 [vocab, d] row-major, f32 accumulation,
+ * written when `logits` is non-NULL), out_max[b] / out_idx[b] = the maximum and
+ * vocab_offset + its row (lowest row on ties).  A rank of a vocab-parallel
+ * group reduces (out_max, out_idx) across ranks instead of gathering logits.
+ * workspace >= qigen_lm_head_workspace_size bytes, zero-filled once before
+ * first use (the kernel leaves it zeroed).  Deterministic for any grid.
+ * Replaces the decode driver's cuBLAS GEMV + argmax (no reference counterpart,
+ * SPEC.md:13). */
+int64_t qigen_lm_head_workspace_size(int64_t vocab, int64_t d, int64_t batch);
+int qigen_lm_head(const float* h, const float* norm_w, float eps, const void* w_f16,
+                  int64_t vocab, int64_t d, int64_t batch, int64_t vocab_offset, float* logits,
+                  float* out_max, int64_t* out_idx, void* workspace, int64_t workspace_bytes,
+                  void* stream);
+
 /* Small-batch quantized GEMM on the tcgen05 tensor cores (north_star (c)):
  * weights dequantized to fp16 (w = s (c - z)) in shared memory, activations
  * converted to fp16, f32 accumulation in TMEM.  4-bit, group 32..256 (dividing

@@ -70,6 +70,21 @@ SIGNATURES = {
     "qigen_attn_decode_workspace_size": (_I64, [_I64, _I64, _I64, _I64]),
     "qigen_attn_decode": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
                                  ctypes.c_float, _P, _P, _I64, _P]),
+    "qigen_tp_buffer_size": (_I64, [_I32, _I64, _I64]),
+    "qigen_tp_alloc": (_I32, [_I64, ctypes.POINTER(_P), _P]),
+    "qigen_tp_free": (_I32, [_P]),
+    "qigen_tp_open_peer": (_I32, [_P, ctypes.POINTER(_P)]),
+    "qigen_tp_close_peer": (_I32, [_P]),
+    "qigen_tp_create": (_I32, [_I32, _I32, _I64, _I64, _I32, _P, ctypes.POINTER(_P)]),
+    "qigen_tp_destroy": (_I32, [_P]),
+    "qigen_tp_step_begin": (_I32, [_P, _P]),
+    "qigen_gemv_tp_push": (_I32, [_P, _I32, _P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64,
+                                  _I32, _P, ctypes.c_float, _P, _I64, _P]),
+    "qigen_tp_reduce": (_I32, [_P, _I32, _I32, _P, _I64, _P]),
+    "qigen_tp_error": (_I32, [_P, ctypes.POINTER(_I32)]),
+    "qigen_lm_head_workspace_size": (_I64, [_I64, _I64, _I64]),
+    "qigen_lm_head": (_I32, [_P, _P, ctypes.c_float, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
+                             _I64, _P]),
     "qigen_gemm_tc_workspace_size": (_I64, [_I64, _I64]),
     "qigen_gemm_tc": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64, _I32,
                              _I32, _P, _I64, _P]),

@@ -35,6 +35,7 @@
 
 #include "common.cuh"
 #include "gemv_common.cuh"
+#include "tp.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -66,6 +67,8 @@ struct GemvArgs {
   unsigned long long* trace_clk;  // optional per-CTA SM clocks at the same points
   int early;                  // trigger dependents at kernel entry
   int policy;                 // 1: weight bulk copies carry an L2 evict_first hint
+  int push_on;                // TP push epilogue: y goes to every rank's inbox (tp.cuh)
+  TpPush push;
 };
 
 __device__ __forceinline__ void trace_point(const GemvArgs& a, int i) {
@@ -625,11 +628,28 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
           if (a.xmode == 3) v *= ssl[tk];
           const int64_t col = col0 + row;
           if (col < a.m) {
-            float* dst = a.y + tk * a.ldy + col;
-            *dst = a.accumulate ? *dst + v : v;
+            if (a.push_on) {  // this rank's partial into every rank's inbox (NVLink stores)
+              const TpPush& pp = a.push;
+              const size_t off = ((size_t)(pp.slot * pp.world + pp.rank) * pp.bmax + tk) * pp.d + col;
+              for (int q = 0; q < pp.world; ++q) pp.inbox[q][off] = v;
+            } else {
+              float* dst = a.y + tk * a.ldy + col;
+              *dst = a.accumulate ? *dst + v : v;
+            }
           }
         }
       }
+    }
+  }
+  if (a.push_on && rank == 0) {
+    // release the pushed columns: every thread's stores are ordered before the
+    // arrival counts (system scope), one count per rank
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const TpPush& pp = a.push;
+      const unsigned ncols = (unsigned)min((int64_t)WPC * 16, a.m - col0);
+      for (int q = 0; q < pp.world; ++q) atomicAdd_system(pp.flags[q] + pp.slot * 8 + pp.rank, ncols);
     }
   }
   trace_point(a, 4);
@@ -932,14 +952,14 @@ extern "C" int64_t qigen_gemv_workspace_size(int64_t n, int64_t tokens) {
   return supersteps(n) * 8 * tp * (128 + 16);  // digits + unit factors (g = 16: 2 units per step)
 }
 
-extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
-                             int64_t group, const void* x, int x_dtype, int64_t tokens,
-                             int64_t ldx, float* y, int64_t ldy, int accumulate, int k_splits,
-                             int prologue, const float* prologue_w, float eps, void* workspace,
-                             int64_t workspace_bytes, void* stream) {
+static int gemv_entry(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+                      int64_t group, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
+                      float* y, int64_t ldy, int accumulate, int k_splits, int prologue,
+                      const float* prologue_w, float eps, void* workspace,
+                      int64_t workspace_bytes, void* stream, const TpPush* push) {
   QIGEN_CHECK_ARG(bits == 2 || bits == 3 || bits == 4, QIGEN_ERR_CONFIG,
                   "bits must be one of (2, 3, 4), got %d", bits);
-  QIGEN_CHECK_ARG(qw && qsz && x && y, QIGEN_ERR_ARG, "null pointer");
+  QIGEN_CHECK_ARG(qw && qsz && x && (y || push), QIGEN_ERR_ARG, "null pointer");
   QIGEN_CHECK_ARG(n > 0 && m > 0, QIGEN_ERR_ARG, "empty matrix");
   QIGEN_CHECK_ARG(group == 0 || (n % group == 0), QIGEN_ERR_CONFIG,
                   "group size %lld does not divide row count %lld", (long long)group, (long long)n);
@@ -985,6 +1005,10 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   a.trace_clk = g_trace_clk;
   a.early = g_early || a.x_ready;  // independent x: overlap the predecessor fully
   a.policy = g_policy;
+  if (push) {
+    a.push_on = 1;
+    a.push = *push;
+  }
   const int S = k_splits;  // 0: chosen per launch shape in launch_cfg
   cudaStream_t s = (cudaStream_t)stream;
 #define QIGEN_LAUNCH(B) \
@@ -995,6 +1019,39 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
     default: QIGEN_LAUNCH(4);
   }
 #undef QIGEN_LAUNCH
+}
+
+extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+                             int64_t group, const void* x, int x_dtype, int64_t tokens,
+                             int64_t ldx, float* y, int64_t ldy, int accumulate, int k_splits,
+                             int prologue, const float* prologue_w, float eps, void* workspace,
+                             int64_t workspace_bytes, void* stream) {
+  return gemv_entry(qw, qsz, n, m, bits, group, x, x_dtype, tokens, ldx, y, ldy, accumulate,
+                    k_splits, prologue, prologue_w, eps, workspace, workspace_bytes, stream,
+                    nullptr);
+}
+
+extern "C" int qigen_gemv_tp_push(const qigen_tp_comm* comm, int slot, const uint32_t* qw,
+                                  const float* qsz, int64_t n, int64_t m, int bits,
+                                  int64_t group, const void* x, int x_dtype, int64_t tokens,
+                                  int64_t ldx, int prologue, const float* prologue_w, float eps,
+                                  void* workspace, int64_t workspace_bytes, void* stream) {
+  QIGEN_CHECK_ARG(comm, QIGEN_ERR_ARG, "null comm");
+  QIGEN_CHECK_ARG(slot == 0 || slot == 1, QIGEN_ERR_ARG, "slot must be 0 or 1");
+  QIGEN_CHECK_ARG(m == comm->d && tokens <= comm->bmax, QIGEN_ERR_ARG,
+                  "push GEMV: m must equal the comm's d and tokens <= its max");
+  TpPush p = {};
+  for (int q = 0; q < comm->world; ++q) {
+    p.flags[q] = (unsigned*)comm->base[q];
+    p.inbox[q] = (float*)((char*)comm->base[q] + kTpHeader);
+  }
+  p.rank = comm->rank;
+  p.world = comm->world;
+  p.slot = slot;
+  p.bmax = comm->bmax;
+  p.d = comm->d;
+  return gemv_entry(qw, qsz, n, m, bits, group, x, x_dtype, tokens, ldx, nullptr, m, 0, 0,
+                    prologue, prologue_w, eps, workspace, workspace_bytes, stream, &p);
 }
 
 extern "C" int qigen_gemv(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,

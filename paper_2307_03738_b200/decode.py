@@ -6,15 +6,28 @@ cache of 512 / 1024 past tokens, tensor-parallel over the GPUs of one node.
 The reference has no model path; this driver is the consumer the
 quantized GEMV exists for.
 
-Sharding (Megatron pairing, one process per GPU, NCCL):
+Sharding (Megatron pairing, one process per GPU):
   * column-parallel, no communication: fused QKV (heads split across ranks) and
     fused gate|up (FFN columns split);
   * row-parallel: o_proj and down_proj take K-shards aligned to whole
     quantization groups and whole 256-row supersteps (uneven when the group
-    count does not divide, e.g. 7B down_proj K = 11008 = 43 supersteps); rank 0
-    accumulates the residual into its partial inside the GEMV epilogue, then
-    one NCCL all-reduce per row-parallel layer (2 per layer);
-  * lm_head is vocab-parallel (fp16), followed by an all-gather of logits.
+    count does not divide, e.g. 7B down_proj K = 11008 = 43 supersteps).  The
+    all-reduce after each (2 per layer) is the one-shot push of csrc/tp.cuh:
+    the GEMV epilogue stores its partial into every rank's inbox over NVLink
+    (CUDA IPC), then a reduce kernel adds the partials to the residual in rank
+    order ("push").  Without peer mappings it falls back
+    to rank 0 accumulating the residual in its GEMV epilogue + an NCCL
+    all-reduce ("nccl");
+  * lm_head is vocab-parallel (fp16) with the RMSNorm and the greedy argmax
+    fused into one kernel per rank (csrc/lmhead.cu); ranks exchange only
+    (max, index) pairs.
+
+The step is a generator of phases (``step_phases``) that yields where a rank
+needs the other ranks' data; ``step`` runs it to the end.  Several ranks can
+therefore be emulated on ONE GPU (``emulated_tp``): every rank's phase k is
+issued before any rank's phase k+1, so no kernel waits on one that has not
+been launched before it (B200_PROFILING.md: ranks that wait on one another
+must not run as separate launches unless their order guarantees progress).
 
 Everything runs inside one CUDA graph per decode step.  The quantized linears
 are ``PanelWeights`` (GPU quantize, bit-exact with quant.py, then the IMMA
@@ -113,6 +126,7 @@ class TP:
         self.group = group
         self.rank = self.dist.get_rank(group) if self.dist else 0
         self.world = self.dist.get_world_size(group) if self.dist else 1
+        self._post = None
 
     def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:
@@ -129,6 +143,29 @@ class TP:
         self.dist.all_gather(outs, pad.contiguous(), group=self.group)
         return torch.cat([o[..., :s] for o, s in zip(outs, sizes)], dim=-1)
 
+    # greedy token across vocab shards: each rank posts (max, global index) per
+    # token, the token is the first rank's index among the maxima (= the lowest
+    # global index, torch.argmax's tie rule over the concatenated logits)
+    def argmax_post(self, mx: torch.Tensor, ix: torch.Tensor, logits=None, sizes=None) -> None:
+        self._post = (mx, ix, logits, sizes)
+
+    def argmax_collect(self):
+        mx, ix, logits, sizes = self._post
+        self._post = None
+        if self.world == 1:
+            return ix, logits
+        pair = torch.stack([mx.double(), ix.double()], dim=-1)  # [B, 2]
+        outs = [torch.empty_like(pair) for _ in range(self.world)]
+        self.dist.all_gather(outs, pair, group=self.group)
+        full = None if logits is None else self.all_gather_cat(logits, sizes)
+        return pick_argmax(torch.stack(outs)), full
+
+
+def pick_argmax(pairs: torch.Tensor) -> torch.Tensor:
+    """pairs [world, B, 2] of (max, global index) -> global argmax per token."""
+    r = pairs[..., 0].argmax(0)  # first maximal rank
+    return pairs[r, torch.arange(pairs.shape[1], device=pairs.device), 1].long()
+
 
 class ShardTP(TP):
     """One rank's shard of a TP group of `world` ranks on a single GPU, with the
@@ -139,12 +176,132 @@ class ShardTP(TP):
     def __init__(self, world: int, rank: int = 0):
         self.dist, self.group = None, None
         self.rank, self.world = rank, world
+        self._post = None
 
     def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
         return t
 
     def all_gather_cat(self, t: torch.Tensor, sizes: list[int]) -> torch.Tensor:
         return F.pad(t, (0, sum(sizes) - t.shape[-1]))
+
+    def argmax_collect(self):
+        mx, ix, logits, sizes = self._post
+        self._post = None
+        return ix, None if logits is None else self.all_gather_cat(logits, sizes)
+
+
+class EmuGroup:
+    """A TP group of `world` ranks emulated in one process on one GPU: the
+    (max, index) / logit exchange goes through shared tensors; the row-parallel
+    all-reduces must use the push comm (TpComm.emulated)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.posts = [None] * world
+
+
+class EmuTP(TP):
+    def __init__(self, group: EmuGroup, rank: int):
+        self.dist, self.group = None, group
+        self.rank, self.world = rank, group.world
+        self._post = None
+
+    def all_reduce(self, t):
+        raise RuntimeError("emulated TP ranks all-reduce through the push comm only")
+
+    def all_gather_cat(self, t, sizes):
+        raise RuntimeError("emulated TP ranks exchange through argmax_post / argmax_collect")
+
+    def argmax_post(self, mx, ix, logits=None, sizes=None) -> None:
+        self.group.posts[self.rank] = (mx, ix, logits)
+
+    def argmax_collect(self):
+        posts = self.group.posts
+        pairs = torch.stack([torch.stack([p[0].double(), p[1].double()], dim=-1) for p in posts])
+        full = None
+        if all(p[2] is not None for p in posts):
+            full = torch.cat([p[2] for p in posts], dim=-1)
+        return pick_argmax(pairs), full
+
+
+class TpComm:
+    """The push all-reduce of csrc/tp.cuh for one rank: its buffer, the peers'
+    buffers mapped into this process, and the C handle."""
+
+    def __init__(self, rank, world, d, bmax, layers, bases, owned=(), opened=()):
+        import ctypes
+        from ._lib import lib
+        self.rank, self.world, self.d, self.bmax = rank, world, d, bmax
+        self._owned, self._opened = list(owned), list(opened)
+        arr = (ctypes.c_void_p * 8)(*[ctypes.c_void_p(b) for b in bases])
+        h = ctypes.c_void_p()
+        call("qigen_tp_create", rank, world, d, bmax, layers, arr, ctypes.byref(h))
+        self._h = h
+        self._lib = lib()
+
+    @staticmethod
+    def _alloc(world, d, bmax, with_handle):
+        import ctypes
+        from ._lib import lib
+        nbytes = int(lib().qigen_tp_buffer_size(world, d, bmax))
+        p = ctypes.c_void_p()
+        hbuf = ctypes.create_string_buffer(64) if with_handle else None
+        call("qigen_tp_alloc", nbytes, ctypes.byref(p), hbuf)
+        return p.value, (hbuf.raw if with_handle else None)
+
+    @classmethod
+    def setup_dist(cls, tp: TP, d, bmax, layers) -> "TpComm":
+        """Real ranks (one process per GPU): allocate, exchange CUDA IPC handles
+        over the process group, map every peer's buffer."""
+        import ctypes
+        base, handle = cls._alloc(tp.world, d, bmax, True)
+        handles = [None] * tp.world
+        tp.dist.all_gather_object(handles, handle, group=tp.group)
+        bases, opened = [], []
+        for q, hq in enumerate(handles):
+            if q == tp.rank:
+                bases.append(base)
+                continue
+            p = ctypes.c_void_p()
+            call("qigen_tp_open_peer", ctypes.create_string_buffer(hq, 64), ctypes.byref(p))
+            bases.append(p.value)
+            opened.append(p.value)
+        tp.dist.barrier(group=tp.group)
+        return cls(tp.rank, tp.world, d, bmax, layers, bases, owned=[base], opened=opened)
+
+    @classmethod
+    def emulated(cls, world, d, bmax, layers) -> list["TpComm"]:
+        """`world` ranks on this GPU: plain device buffers, each rank's peers are
+        the other ranks' buffers."""
+        bases = [cls._alloc(world, d, bmax, False)[0] for _ in range(world)]
+        comms = [cls(r, world, d, bmax, layers, bases) for r in range(world)]
+        comms[0]._owned = bases
+        return comms
+
+    def step_begin(self) -> None:
+        call("qigen_tp_step_begin", self._h, _dev.stream_handle())
+
+    def reduce(self, slot: int, layer: int, h: torch.Tensor) -> None:
+        call("qigen_tp_reduce", self._h, slot, layer, h.data_ptr(), h.shape[0],
+             _dev.stream_handle())
+
+    def error(self) -> int:
+        import ctypes
+        v = ctypes.c_int()
+        call("qigen_tp_error", self._h, ctypes.byref(v))
+        return v.value
+
+    def __del__(self):
+        try:
+            lib_ = self._lib
+            for p in getattr(self, "_opened", []):
+                lib_.qigen_tp_close_peer(p)
+            for p in getattr(self, "_owned", []):
+                lib_.qigen_tp_free(p)
+            if getattr(self, "_h", None):
+                lib_.qigen_tp_destroy(self._h)
+        except Exception:  # noqa: BLE001
+            pass
 
 
 # ---------------------------------------------------------------------------
@@ -162,6 +319,10 @@ class GpuLinear:
                  prologue: str | None = None, norm_weight=None, eps: float = 1e-5) -> torch.Tensor:
         return self.pw.gemv(x, out=out, accumulate=accumulate, prologue=prologue,
                             norm_weight=norm_weight, eps=eps)
+
+    def push(self, comm: "TpComm", slot: int, x: torch.Tensor, prologue: str | None = None):
+        """Row-parallel partial x W into every rank's inbox (qigen_gemv_tp_push)."""
+        self.pw.push(comm, slot, x, prologue=prologue)
 
     @property
     def nbytes(self) -> int:
@@ -199,17 +360,37 @@ class GpuBackend:
         call("qigen_rmsnorm_f16", h.data_ptr(), w.data_ptr(), h.shape[0], h.shape[1], float(eps),
              out.data_ptr(), _dev.stream_handle())
 
+    @staticmethod
+    def lm_head_workspace(V, d, B, device):
+        from ._lib import lib
+        n = int(lib().qigen_lm_head_workspace_size(V, d, B))
+        return torch.zeros(n, dtype=torch.uint8, device=device)
+
+    @staticmethod
+    def lm_head(h, norm_w, eps, w_f16, v0, logits, mx, ix, workspace):
+        """Final RMSNorm + fp16 vocab-shard GEMV + greedy argmax, one kernel
+        (csrc/lmhead.cu): mx / ix get each token's max logit and global index."""
+        call("qigen_lm_head", h.data_ptr(), norm_w.data_ptr(), float(eps), w_f16.data_ptr(),
+             w_f16.shape[0], w_f16.shape[1], h.shape[0], int(v0),
+             None if logits is None else logits.data_ptr(), mx.data_ptr(), ix.data_ptr(),
+             workspace.data_ptr(), workspace.numel(), _dev.stream_handle())
+
 
 # ---------------------------------------------------------------------------
 # the model
 # ---------------------------------------------------------------------------
 
 class LlamaTP:
-    """One tensor-parallel shard of a random-init LLaMA-architecture model."""
+    """One tensor-parallel shard of a random-init LLaMA-architecture model.
+
+    ``comm``: how the row-parallel all-reduces run when world > 1 —
+    ``"auto"`` (the push comm over CUDA IPC when the backend is the GPU one and
+    the peers map, else NCCL), ``"push"``, ``"nccl"``, or a ``TpComm`` (emulated
+    ranks).  ``keep_logits``: also assemble the full logits (``last_logits``)."""
 
     def __init__(self, cfg: LlamaConfig, *, batch: int = 1, max_ctx: int = 1024, seed: int = 0,
                  device=None, tp: TP | None = None, backend=GpuBackend,
-                 kv_dtype=torch.float16):
+                 kv_dtype=torch.float16, comm="auto", keep_logits: bool = True):
         self.cfg, self.B, self.max_ctx = cfg, batch, max_ctx
         self.tp = tp or TP()
         self.dev = torch.device(device) if device is not None else torch.device("cuda")
@@ -286,6 +467,25 @@ class LlamaTP:
                 cache[li] = g[:, self.h0:self.h1].to(kv_dtype)
                 del g
         self.attn_ws = backend.attention_workspace(batch, self.nh, hd, max_ctx, self.dev)
+        self.keep_logits = keep_logits
+        self.fused_head = hasattr(backend, "lm_head") and self.dev.type == "cuda" and batch <= 8
+        if self.fused_head:
+            self.head_ws = backend.lm_head_workspace(self.v1 - self.v0, d, batch, self.dev)
+        # row-parallel all-reduce: the push comm (csrc/tp.cuh) or NCCL
+        self.comm, self.comm_kind = None, None
+        if self.tp.world > 1:
+            if isinstance(comm, TpComm):
+                self.comm, self.comm_kind = comm, "push (emulated ranks)"
+            elif comm in ("auto", "push") and backend is GpuBackend and self.tp.dist is not None:
+                try:
+                    self.comm = TpComm.setup_dist(self.tp, d, batch, cfg.n_layers)
+                    self.comm_kind = "push (one-shot, GEMV epilogue -> peer inboxes over NVLink)"
+                except Exception as e:  # noqa: BLE001
+                    if comm == "push":
+                        raise
+                    self.comm_kind = f"nccl (push setup failed: {type(e).__name__})"
+            else:
+                self.comm_kind = "nccl"
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device=self.dev).float() / hd))
         ang = torch.arange(max_ctx, device=self.dev).float()[:, None] * inv[None, :]
         self.cos, self.sin = ang.cos(), ang.sin()  # [ctx, hd/2]
@@ -304,13 +504,23 @@ class LlamaTP:
     # -- one decode step ----------------------------------------------------
     def step(self, tokens: torch.Tensor, pos: int) -> torch.Tensor:
         """Greedy next tokens for `tokens` [B] at position `pos` (static shapes:
-        graph-capturable for a fixed pos).  Per layer: QKV GEMV (RMSNorm fused:
-        folded into W with 1/rms in the epilogue at 1-2 tokens, else a prologue)
-        -> fused RoPE + KV append + attention -> o_proj GEMV (residual fused,
-        all-reduce) -> gate|up GEMV (RMSNorm prologue) -> down GEMV (SwiGLU
-        fused, residual fused, all-reduce)."""
+        graph-capturable for a fixed pos)."""
+        for _ in self.step_phases(tokens, pos):
+            pass
+        return self.next_tokens
+
+    def step_phases(self, tokens: torch.Tensor, pos: int):
+        """The decode step as phases; yields where the other ranks' data is
+        needed next.  Per layer: QKV GEMV (RMSNorm fused: folded into W with
+        1/rms in the epilogue at 1-2 tokens, else a prologue) -> fused RoPE + KV
+        append + attention -> o_proj GEMV (+ all-reduce with the residual) ->
+        gate|up GEMV (RMSNorm prologue) -> down GEMV (SwiGLU prologue, +
+        all-reduce with the residual); then the fused final RMSNorm + LM head +
+        argmax."""
         cfg, B, hd, be = self.cfg, self.B, self.cfg.head_dim, self.backend
         h = self.embed[tokens].float()                     # [B, d] residual stream
+        if self.comm is not None:
+            self.comm.step_begin()
         cos, sin = self.cos[pos], self.sin[pos]
         scale = 1.0 / math.sqrt(hd)
         att = torch.empty((B, self.nh * hd), dtype=torch.float32, device=self.dev)
@@ -322,26 +532,75 @@ class LlamaTP:
             # RoPE + KV append + attention over positions 0..pos
             be.attention(qkv, cos, sin, self.k_cache[li], self.v_cache[li], pos, scale, att,
                          self.attn_ws)
-            h = self._row_parallel(lay["o"], att, h)
+            yield from self._row_parallel(lay["o"], att, h, None, 0, li)
             gu = lay["gu"](h, prologue="rmsnorm", norm_weight=lay["n2"], eps=cfg.norm_eps)
-            h = self._row_parallel(lay["down"], gu, h, prologue="swiglu")
-        xn = torch.empty((B, cfg.d_model), dtype=torch.float16, device=self.dev)
-        be.rmsnorm_f16(h, self.norm, cfg.norm_eps, xn)
-        logits = (xn @ self.lm_head.t()).float()           # [B, V_l]
-        logits = self.tp.all_gather_cat(logits, self.v_sizes)
-        self.last_logits = logits
-        return logits.argmax(-1)
+            yield from self._row_parallel(lay["down"], gu, h, "swiglu", 1, li)
+        Vl = self.v1 - self.v0
+        if self.fused_head:
+            logits = (torch.empty((B, Vl), dtype=torch.float32, device=self.dev)
+                      if self.keep_logits else None)
+            mx = torch.empty(B, dtype=torch.float32, device=self.dev)
+            ix = torch.empty(B, dtype=torch.int64, device=self.dev)
+            be.lm_head(h, self.norm, cfg.norm_eps, self.lm_head, self.v0, logits, mx, ix,
+                       self.head_ws)
+        else:
+            xn = torch.empty((B, cfg.d_model), dtype=torch.float16, device=self.dev)
+            be.rmsnorm_f16(h, self.norm, cfg.norm_eps, xn)
+            logits = (xn.double() @ self.lm_head.double().t()).float()   # [B, V_l]
+            mx, ix = logits.max(-1)
+            ix = ix + self.v0
+        self.tp.argmax_post(mx, ix, logits if self.keep_logits else None, self.v_sizes)
+        yield
+        self.next_tokens, self.last_logits = self.tp.argmax_collect()
 
-    def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor, prologue=None) -> torch.Tensor:
-        """Row-parallel linear + residual: rank 0 accumulates its partial into h
-        inside the GEMV epilogue, the other ranks produce bare partials, and one
-        all-reduce forms h + sum of partials on every rank."""
+    def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor, prologue, slot: int,
+                      layer: int):
+        """Row-parallel linear + residual, h updated in place.  World 1: the GEMV
+        adds its output to h in its epilogue.  Push comm: every rank's GEMV
+        stores its partial into every rank's inbox, then (after the phase
+        boundary) each rank adds the partials to h in rank order.  NCCL: rank 0
+        accumulates into h, the others produce bare partials, one all-reduce."""
+        if self.tp.world == 1:
+            lin(x, out=h, accumulate=True, prologue=prologue)
+            return
+        if self.comm is not None:
+            lin.push(self.comm, slot, x, prologue=prologue)
+            yield
+            self.comm.reduce(slot, layer, h)
+            return
         if self.tp.rank == 0:
             lin(x, out=h, accumulate=True, prologue=prologue)
-            out = h
+            self.tp.all_reduce(h)
         else:
-            out = lin(x, prologue=prologue)
-        return self.tp.all_reduce(out)
+            h.copy_(self.tp.all_reduce(lin(x, prologue=prologue)))
+        return
+        yield  # (generator)
+
+
+def emulated_tp(cfg: LlamaConfig, world: int, **kw) -> list[LlamaTP]:
+    """`world` TP ranks of one model on THIS GPU (for tests and per-rank
+    measurements): one LlamaTP shard per rank, the push comm over plain device
+    buffers.  Drive them with ``emulated_step``."""
+    group = EmuGroup(world)
+    comms = TpComm.emulated(world, cfg.d_model, kw.get("batch", 1), cfg.n_layers)
+    return [LlamaTP(cfg, tp=EmuTP(group, r), comm=comms[r], **kw) for r in range(world)]
+
+
+def emulated_step(models: list[LlamaTP], tokens: torch.Tensor, pos: int) -> torch.Tensor:
+    """One decode step of emulated ranks: every rank's phase k is issued before
+    any rank's phase k+1 (all on the current stream), so a reduce only ever
+    waits for pushes launched before it."""
+    gens = [m.step_phases(tokens, pos) for m in models]
+    live = True
+    while live:
+        live = False
+        for g in gens:
+            try:
+                next(g)
+                live = True
+            except StopIteration:
+                pass
+    return models[0].next_tokens
 
 
 def shrink(cfg: LlamaConfig, **kw) -> LlamaConfig:

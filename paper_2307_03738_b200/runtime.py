@@ -227,6 +227,25 @@ class PanelWeights:
         return out.reshape(self.m) if squeeze else out
 
 
+    def push(self, comm, slot: int, x: torch.Tensor, *, prologue: str | None = None,
+             norm_weight: torch.Tensor | None = None, eps: float = 1e-5) -> None:
+        """Row-parallel partial x W of a tensor-parallel rank, stored by the GEMV
+        epilogue into slot `slot` of every rank's inbox (qigen_gemv_tp_push;
+        the reduce is ``comm.reduce``).  x: CUDA [tokens, n] (or [tokens, 2n]
+        for the SwiGLU prologue)."""
+        x2 = x.reshape(1, -1) if x.dim() == 1 else x
+        width = 2 * self.n if prologue == "swiglu" else self.n
+        if x2.dim() != 2 or x2.shape[1] != width or x2.dtype not in _DTYPES or x2.stride(1) != 1:
+            raise ConfigError(f"x must be a unit-stride CUDA [tokens, {width}] f32/f16/bf16 tensor")
+        mode = {None: 0, "rmsnorm": 1, "swiglu": 2}[prologue]
+        T = x2.shape[0]
+        ws = self._workspace(min(T, MAX_GEMV_TOKENS), x2.device)
+        call("qigen_gemv_tp_push", comm._h, int(slot), self.qw.data_ptr(), self.qsz.data_ptr(),
+             self.n, self.m, self.bits, self.group_code, x2.data_ptr(), _DTYPES[x2.dtype], T,
+             x2.stride(0), mode, norm_weight.data_ptr() if mode == 1 else None, float(eps),
+             ws.data_ptr(), ws.numel(), _dev.stream_handle())
+
+
 X_READY = 2  # QIGEN_GEMV_X_READY (include/qigen_b200.h)
 
 

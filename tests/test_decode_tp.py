@@ -183,3 +183,78 @@ def test_shard_tp_is_a_compute_only_stand_in():
     assert m.nh == TINY.n_heads // 4
     out = m.step(torch.tensor([3]), pos=2)
     assert tuple(out.shape) == (1,)
+
+
+# --- fused LM head and the push all-reduce (GPU) ------------------------------
+
+def _lm_ref(h, nw, W, eps=1e-5):
+    xn = (h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + eps) * nw).half()
+    return xn.double() @ W.double().t()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V,d,B", [(32000, 4096, 1), (32000, 8192, 8), (4000, 4096, 1),
+                                   (4000, 8192, 8), (16000, 4096, 3), (1005, 512, 2), (7, 1024, 1)])
+def test_lm_head_kernel(V, d, B):
+    """qigen_lm_head (final RMSNorm + fp16 GEMV + greedy argmax) against a
+    float64 torch reference: logits within 2e-3 of max|logit| (same fp16
+    activation rounding up to one ulp), the returned (max, index) is the exact
+    argmax of the kernel's own logits (lowest index on ties), and equals the
+    reference argmax whenever the reference's top-2 gap exceeds the tolerance.
+    Small shards exercise the cross-CTA K split; repeated launches reuse the
+    workspace (its counters return to zero)."""
+    g = torch.Generator(device="cuda").manual_seed(V + d + B)
+    h = torch.randn(B, d, device="cuda", generator=g) * 3
+    nw = torch.rand(d, device="cuda", generator=g) + 0.5
+    W = (torch.randn(V, d, device="cuda", generator=g) * 0.02).half()
+    ws = D.GpuBackend.lm_head_workspace(V, d, B, "cuda")
+    ref = _lm_ref(h, nw, W)
+    for v0 in (0, 123456):
+        logits = torch.empty(B, V, device="cuda")
+        mx = torch.empty(B, device="cuda")
+        ix = torch.empty(B, dtype=torch.int64, device="cuda")
+        D.GpuBackend.lm_head(h, nw, 1e-5, W, v0, logits, mx, ix, ws)
+        torch.cuda.synchronize()
+        assert ((logits.double() - ref).abs().max() / ref.abs().max()).item() < 2e-3
+        own = logits.argmax(-1)
+        assert torch.equal(ix - v0, own)
+        assert torch.equal(mx, logits.gather(1, own[:, None])[:, 0])
+        top2 = ref.topk(min(2, V), dim=-1).values
+        clear = (top2[:, 0] - top2[:, -1]) > 4e-3 * ref.abs().max()
+        assert torch.equal((ix - v0)[clear], ref.argmax(-1)[clear])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,cfg", [(2, "small"), (4, "small"), (4, "7b2")])
+def test_emulated_tp_push_matches_tp1(world, cfg):
+    """The push all-reduce (GEMV epilogue -> every rank's inbox, reduce in rank
+    order) with `world` ranks emulated on this GPU, against TP=1 of the same
+    model: same greedy tokens, logits within 5e-4 of max|logit| (TP changes the
+    f32 summation order of h; the LM head rounds RMSNorm(h) to fp16, 2^-11
+    relative, before its GEMV), no wait timed out, and two
+    consecutive steps (the epoch-based counters advance).  "7b2" is 2 layers
+    at full 7B width (uneven down_proj K-shards at TP 4)."""
+    if cfg == "small":
+        c = D.LlamaConfig(n_layers=3, d_model=512, n_heads=8, head_dim=64, ffn=1536, vocab=1000,
+                          bits=4, group=64)
+        B, ctx = 2, 48
+    else:
+        c, B, ctx = D.shrink(D.LLAMA_7B, n_layers=2), 1, 512
+    ref = D.LlamaTP(c, batch=B, max_ctx=ctx + 2, seed=11, device="cuda")
+    models = D.emulated_tp(c, world, batch=B, max_ctx=ctx + 2, seed=11, device="cuda")
+    tok = (torch.arange(B, device="cuda") * 37 + 5) % c.vocab
+    for step in range(2):
+        t1 = ref.step(tok, ctx + step)
+        tn = D.emulated_step(models, tok, ctx + step)
+        torch.cuda.synchronize()
+        l1, ln = ref.last_logits.double(), models[0].last_logits.double()
+        assert ln.shape == l1.shape
+        assert ((ln - l1).abs().max() / (1 + l1.abs().max())).item() < 5e-4, step
+        assert torch.equal(tn, t1), step
+        assert all(torch.equal(m.next_tokens, tn) for m in models)
+        tok = t1
+    assert all(m.comm.error() == 0 for m in models)
+    # the KV caches of each rank's heads got the same rows as TP=1
+    for m in models:
+        assert torch.allclose(m.k_cache[:, :, :, ctx].float(),
+                              ref.k_cache[:, :, m.h0:m.h1, ctx].float(), atol=2e-3, rtol=2e-3)
