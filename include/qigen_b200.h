@@ -141,6 +141,33 @@ int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, in
                   const float* prologue_w, float eps, void* workspace, int64_t workspace_bytes,
                   void* stream);
 
+/* Dependent GEMV chains of the decode driver without activation prep kernels.
+ * A PRODUCER GEMV (y_digits set) writes its final output columns (after the
+ * residual add) twice: as y, and as the prepared activation digits of the
+ * consumer GEMV whose K is this m (times out_scale[col], e.g. the consumer's
+ * RMSNorm weight), together with per-CTA sums of squares of y in
+ * ss_out[t * qigen_gemv_ss_count(m) + cta].  The CONSUMER (x_digits set) reads
+ * those digits instead of x (no prologue, no prep kernel) and, with ss_in,
+ * applies the RMSNorm's 1 / rms = rsqrt(sum_c ss_in[t * ss_count + c] / n + eps)
+ * in its epilogue (fixed summation order).  Digit buffers are
+ * qigen_gemv_workspace_size(K, tokens) bytes, zero-filled once; producer and
+ * consumer use the same token count.  Consumer group sizes 32..256 / FC. */
+typedef struct {
+  const void* x_digits;   /* consumer: prepared digits (or NULL: x as usual) */
+  const float* ss_in;     /* consumer: producer's sums of squares (or NULL) */
+  int ss_count;
+  float eps;
+  void* y_digits;         /* producer: consumer's digit buffer (or NULL) */
+  const float* out_scale; /* producer: per-column multiplier (or NULL) */
+  int64_t out_group;      /* producer: consumer's group size (0 = FC) */
+  float* ss_out;          /* producer: sums of squares of y per CTA (or NULL) */
+} qigen_gemv_chain_opts;
+int64_t qigen_gemv_ss_count(int64_t m);
+int qigen_gemv_chain(const uint32_t* qw, const float* qsz, int64_t n, int64_t m, int bits,
+                     int64_t group_size, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
+                     float* y, int64_t ldy, int accumulate, int prologue, const float* prologue_w,
+                     float eps, void* workspace, int64_t workspace_bytes,
+                     const qigen_gemv_chain_opts* opts, void* stream);
 
 /* ---- grouped GEMV: many independent GEMVs in one persistent launch ----------
  * Replaces a sequence of independent qgemv(pm_i, x_i) calls of the reference

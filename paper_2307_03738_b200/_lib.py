@@ -31,6 +31,12 @@ _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int
 
+class ChainOpts(ctypes.Structure):
+    """qigen_gemv_chain_opts (include/qigen_b200.h)."""
+    _fields_ = [("x_digits", _P), ("ss_in", _P), ("ss_count", _I32), ("eps", ctypes.c_float),
+                ("y_digits", _P), ("out_scale", _P), ("out_group", _I64), ("ss_out", _P)]
+
+
 class GemvDesc(ctypes.Structure):
     """qigen_gemv_desc (include/qigen_b200.h)."""
     _fields_ = [("qw", _P), ("qsz", _P), ("n", _I64), ("m", _I64), ("bits", _I32),
@@ -70,6 +76,9 @@ SIGNATURES = {
     "qigen_attn_decode_workspace_size": (_I64, [_I64, _I64, _I64, _I64]),
     "qigen_attn_decode": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
                                  ctypes.c_float, _P, _P, _I64, _P]),
+    "qigen_gemv_ss_count": (_I64, [_I64]),
+    "qigen_gemv_chain": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64,
+                                _I32, _I32, _P, ctypes.c_float, _P, _I64, _P, _P]),
     "qigen_tp_buffer_size": (_I64, [_I32, _I64, _I64]),
     "qigen_tp_alloc": (_I32, [_I64, ctypes.POINTER(_P), _P]),
     "qigen_tp_free": (_I32, [_P]),

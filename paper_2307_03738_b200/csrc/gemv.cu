@@ -69,6 +69,18 @@ struct GemvArgs {
   int policy;                 // 1: weight bulk copies carry an L2 evict_first hint
   int push_on;                // TP push epilogue: y goes to every rank's inbox (tp.cuh)
   TpPush push;
+  // decode chains (qigen_gemv_chain): the producer's epilogue writes its final
+  // output columns (after the residual add) also as the NEXT GEMV's prepared
+  // activation digits, scaled per column by dout_w (that GEMV's RMSNorm weight),
+  // plus per-CTA sums of squares; the consumer bulk-copies the digits (no prep
+  // kernel, no prologue) and applies 1 / rms from the sums in its epilogue.
+  unsigned char* dout;        // consumer's digit buffer (act_prep layout) or null
+  const float* dout_w;        // per-column multiplier or null
+  int dout_tp, dout_ks, dout_ipu;  // consumer's token padding, supersteps, items per unit
+  float* ss_out;              // [M][gridDim.x] sums of squares of the output (or null)
+  const float* ss_in;         // consumer: [M][ss_n] partial sums of squares of its x (or null)
+  int ss_n;
+  int prepared;               // x is already digits at `dig` (skip prep / prologue)
 };
 
 __device__ __forceinline__ void trace_point(const GemvArgs& a, int i) {
@@ -260,9 +272,9 @@ constexpr int kMaxRounds3 = 16;  // xmode 3: prologue rounds of the block per ch
 
 // Shared-memory carve-up (bytes), identical on host and device.
 struct SmemLayout {
-  int ring, bars, bfrag, xs, zero, rbar, pbar, inv, ssw, yp, total, stage;
+  int ring, bars, bfrag, xs, zero, rbar, pbar, inv, ssw, yp, ep, total, stage;
   __host__ __device__ SmemLayout(int bits, int szb, int D, int max_steps, int TP, int M, int WPC,
-                                 int S) {
+                                 int S, int epi = 0) {
     stage = bits * 512 + szb;
     // units are >= 32 rows, except g = 16 (szb 2048: 16 groups per superstep)
     const int max_units = szb == 16 * 128 ? 2 * max_steps : max_steps;
@@ -277,6 +289,7 @@ struct SmemLayout {
     inv = off;   off += 16 * 4;
     ssw = off;   off += kMaxRounds3 * WPC * 8;            // xmode 3: (sum x^2, token) per round x warp
     yp = off;    off += (S - 1) * (WPC * 16 * M + M) * 4 + 16;  // owner's inbox (+ sum x^2 per rank)
+    ep = off;    off += epi ? (2 * M + 1) * WPC * 16 * 4 : 0;  // epilogue: final / old y / scale
     total = off;
   }
 };
@@ -309,7 +322,7 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   const int M = a.M, D = a.D;
   const int nsteps = nks * 8;
   const int nunits = nks * UPS;
-  SmemLayout L(BITS, SZB, D, a.max_steps, TP, M, WPC, S);
+  SmemLayout L(BITS, SZB, D, a.max_steps, TP, M, WPC, S, a.dout != nullptr || a.accumulate);
   unsigned char* ring = smem + L.ring + warp * D * L.stage;
   uint64_t* bars = (uint64_t*)(smem + L.bars) + warp * D;
   float2* xs = (float2*)(smem + L.xs);
@@ -380,6 +393,24 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
   trace_point(a, 9);
   if (!early_x) asm volatile("griddepcontrol.wait;" ::: "memory");
   trace_point(a, 1);
+  // the epilogue's inputs that are not computed here (the y it accumulates
+  // into, the next GEMV's per-column scale), staged now so the epilogue of the
+  // owning CTA does no dependent global loads
+  constexpr int C = WPC * 16;
+  float* ep_fin = (float*)(smem + L.ep);
+  float* ep_old = ep_fin + M * C;
+  float* ep_w = ep_old + M * C;
+  const bool ep_stage = ys == 0 && !early_x && (a.dout || a.accumulate);
+  if (ep_stage) {
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    for (int i = threadIdx.x; i < M * C; i += T) {
+      const int64_t col = c0 + i % C;
+      ep_old[i] = a.accumulate && col < a.m ? a.y[(i / C) * a.ldy + col] : 0.f;
+    }
+    if (a.dout)
+      for (int i = threadIdx.x; i < C; i += T)
+        ep_w[i] = a.dout_w && c0 + i < a.m ? __ldg(a.dout_w + c0 + i) : 1.f;
+  }
 
   // ---- 3. activation digits for this chunk into shared memory ----------------
   if (a.dig) {
@@ -608,6 +639,15 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     }
     __syncthreads();
   }
+  if (a.ss_in && rank == 0) {  // RMSNorm of x folded: 1 / rms from the producer's sums
+    float* invs = (float*)(smem + L.inv);
+    if (threadIdx.x < M) {
+      float ss = 0.f;
+      for (int c = 0; c < a.ss_n; ++c) ss += a.ss_in[threadIdx.x * a.ss_n + c];
+      invs[threadIdx.x] = rsqrtf(ss / (float)a.n + a.eps);
+    }
+    __syncthreads();
+  }
   if (early_x && rank == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before y
   trace_point(a, 7);
 #pragma unroll
@@ -626,7 +666,10 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
         } else {
           for (int q = 1; q < S; ++q) v += yp[(q - 1) * R + e];
           if (a.xmode == 3) v *= ssl[tk];
+          if (a.ss_in) v *= ((const float*)(smem + L.inv))[tk];
           const int64_t col = col0 + row;
+          const float fin = ep_stage ? ep_old[tk * C + row] + v : v;  // (ep_old 0 unless accumulate)
+          if (a.dout) ep_fin[tk * C + row] = col < a.m ? fin : 0.f;
           if (col < a.m) {
             if (a.push_on) {  // this rank's partial into every rank's inbox (NVLink stores)
               const TpPush& pp = a.push;
@@ -634,11 +677,46 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
               for (int q = 0; q < pp.world; ++q) pp.inbox[q][off] = v;
             } else {
               float* dst = a.y + tk * a.ldy + col;
-              *dst = a.accumulate ? *dst + v : v;
+              *dst = ep_stage ? fin : (a.accumulate ? *dst + v : v);
             }
           }
         }
       }
+    }
+  }
+  if (a.dout && rank == 0) {
+    // The CTA's WPC * 16 final columns are rows [col0, col0 + WPC * 16) of the
+    // next GEMV's K: digitise them in the act_prep layout (item it = 4 rows:
+    // step it >> 3, sub-item it & 7), dout_ipu items per exponent unit, and
+    // publish this CTA's sum of squares per token.
+    __syncthreads();
+    const float* ev = ep_fin;
+    for (int tk = warp; tk < M; tk += WPC) {  // (WPC = 8: one warp-wide unit set per token)
+      const int it_l = lane;
+      const int kl = 32 * (it_l >> 3) + 16 * ((it_l & 7) >> 2) + 4 * (it_l & 3);
+      float v4[4], ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float f = ev[tk * C + kl + i];
+        ss += f * f;
+        v4[i] = f * ep_w[kl + i];
+      }
+      Digits d;
+      if (a.dout_ipu == 32) {
+        d = digitize<32>(v4, 0xffffffffu);
+      } else if (a.dout_ipu == 16) {
+        d = digitize<16>(v4, 0xffffu << (lane & 16));
+      } else {
+        d = digitize<8>(v4, 0xffu << (lane & 24));
+      }
+      const int it = (int)(col0 / 4) + it_l;
+      store_digits((uint32_t*)a.dout, it >> 3, tk, a.dout_tp, it & 7, d);
+      if ((it % a.dout_ipu) == 0)
+        ((float2*)(a.dout + (size_t)a.dout_ks * 8 * a.dout_tp * 128))[(it / a.dout_ipu) * a.dout_tp + tk] =
+            make_float2(d.xsum, d.scale);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (a.ss_out && lane == 0) a.ss_out[tk * gridDim.x + blockIdx.x] = ss;
     }
   }
   if (a.push_on && rank == 0) {
@@ -733,11 +811,12 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   auto shape = [&](int S) {  // smem plan for S chunks: ring of <= 80 KB per CTA
     const int max_ks = (a.KS + S - 1) / S;
     a.max_steps = max_ks * 8;
-    SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, TP, a.M, WPC, S);
+    const int epi = a.dout != nullptr || a.accumulate;
+    SmemLayout L0(BITS, GPS * 128, 0, a.max_steps, TP, a.M, WPC, S, epi);
     const int budget = std::min(g_ring_kb ? g_ring_kb * 1024 : WPC * 10 * 1024,
                                 224 * 1024 - L0.total - WPC * 16);
     a.D = std::max(2, std::min(max_ks, budget / (WPC * stage)));
-    return SmemLayout(BITS, GPS * 128, a.D, a.max_steps, TP, a.M, WPC, S);
+    return SmemLayout(BITS, GPS * 128, a.D, a.max_steps, TP, a.M, WPC, S, epi);
   };
   const int cols = (a.P + WPC - 1) / WPC;
   int S = req_S;
@@ -822,7 +901,9 @@ static int launch_cfg(GemvArgs& a, int req_S, cudaStream_t stream) {
   // than every CTA re-reading the row on the 7B chain; slower at 8 tokens)
   const bool norm_prep = a.xmode == 1 && a.M <= 2 && a.KS * 64 <= kNormPrepThreads * kNormPrepMaxR &&
                          (rounds > 2 || g_force_prep || g_norm_prep);
-  if (a.xmode != 3 && (rounds > 2 || g_force_prep || norm_prep)) {
+  if (a.prepared) {
+    a.dig = a.ws;  // digits written by the producer's epilogue (qigen_gemv_chain)
+  } else if (a.xmode != 3 && (rounds > 2 || g_force_prep || norm_prep)) {
     const size_t bytes = (size_t)a.KS * 8 * TP * 128 + (size_t)a.KS * UPS * TP * 8;
     if (a.ws && a.ws_bytes >= bytes) {
       a.dig = a.ws;
@@ -956,10 +1037,12 @@ static int gemv_entry(const uint32_t* qw, const float* qsz, int64_t n, int64_t m
                       int64_t group, const void* x, int x_dtype, int64_t tokens, int64_t ldx,
                       float* y, int64_t ldy, int accumulate, int k_splits, int prologue,
                       const float* prologue_w, float eps, void* workspace,
-                      int64_t workspace_bytes, void* stream, const TpPush* push) {
+                      int64_t workspace_bytes, void* stream, const TpPush* push,
+                      const qigen_gemv_chain_opts* ch = nullptr) {
   QIGEN_CHECK_ARG(bits == 2 || bits == 3 || bits == 4, QIGEN_ERR_CONFIG,
                   "bits must be one of (2, 3, 4), got %d", bits);
-  QIGEN_CHECK_ARG(qw && qsz && x && (y || push), QIGEN_ERR_ARG, "null pointer");
+  const bool prepared = ch && ch->x_digits;
+  QIGEN_CHECK_ARG(qw && qsz && (x || prepared) && (y || push), QIGEN_ERR_ARG, "null pointer");
   QIGEN_CHECK_ARG(n > 0 && m > 0, QIGEN_ERR_ARG, "empty matrix");
   QIGEN_CHECK_ARG(group == 0 || (n % group == 0), QIGEN_ERR_CONFIG,
                   "group size %lld does not divide row count %lld", (long long)group, (long long)n);
@@ -1009,10 +1092,43 @@ static int gemv_entry(const uint32_t* qw, const float* qsz, int64_t n, int64_t m
     a.push_on = 1;
     a.push = *push;
   }
+  if (ch) {
+    if (prepared) {
+      QIGEN_CHECK_ARG(prologue == 0, QIGEN_ERR_ARG, "prepared digits take no prologue");
+      QIGEN_CHECK_ARG(group != 16, QIGEN_ERR_UNSUPPORTED, "prepared digits: group size 16");
+      a.prepared = 1;
+      a.ws = (unsigned char*)ch->x_digits;
+      a.ws_bytes = (size_t)qigen_gemv_workspace_size(n, tokens);
+      a.x = ch->x_digits;
+      a.x_ready = 0;
+      a.early = g_early;
+    }
+    if (ch->ss_in) {
+      QIGEN_CHECK_ARG(prologue != 3 && ch->ss_count > 0, QIGEN_ERR_ARG, "bad ss_in");
+      a.ss_in = ch->ss_in;
+      a.ss_n = ch->ss_count;
+      a.eps = ch->eps;
+    }
+    if (ch->y_digits) {
+      const int64_t og = ch->out_group;
+      QIGEN_CHECK_ARG(og == 0 || og == 32 || og == 64 || og == 128 || og % kSuper == 0,
+                      QIGEN_ERR_UNSUPPORTED, "digit epilogue: consumer group size %lld",
+                      (long long)og);
+      QIGEN_CHECK_ARG(!push, QIGEN_ERR_ARG, "digit epilogue and TP push are exclusive");
+      const int nb = (int)(tokens + 1) / 2;
+      a.dout = (unsigned char*)ch->y_digits;
+      a.dout_w = ch->out_scale;
+      a.dout_tp = 2 * (nb <= 1 ? 1 : nb <= 2 ? 2 : nb <= 4 ? 4 : 8);
+      a.dout_ks = (int)supersteps(m);
+      a.dout_ipu = (og == 32 ? 32 : og == 64 ? 64 : 128) / 4;
+      a.ss_out = ch->ss_out;
+    }
+  }
   const int S = k_splits;  // 0: chosen per launch shape in launch_cfg
   cudaStream_t s = (cudaStream_t)stream;
-#define QIGEN_LAUNCH(B) \
-  return (g_wpc == 16 && tokens <= 4) ? launch_nb<B, 16>(a, S, s) : launch_nb<B, 8>(a, S, s)
+#define QIGEN_LAUNCH(B)                                                              \
+  return (g_wpc == 16 && tokens <= 4 && !a.dout) ? launch_nb<B, 16>(a, S, s)       \
+                                                 : launch_nb<B, 8>(a, S, s)
   switch (bits) {
     case 2: QIGEN_LAUNCH(2);
     case 3: QIGEN_LAUNCH(3);
@@ -1029,6 +1145,18 @@ extern "C" int qigen_gemv_ex(const uint32_t* qw, const float* qsz, int64_t n, in
   return gemv_entry(qw, qsz, n, m, bits, group, x, x_dtype, tokens, ldx, y, ldy, accumulate,
                     k_splits, prologue, prologue_w, eps, workspace, workspace_bytes, stream,
                     nullptr);
+}
+
+extern "C" int64_t qigen_gemv_ss_count(int64_t m) { return (panels(m) + 7) / 8; }
+
+extern "C" int qigen_gemv_chain(const uint32_t* qw, const float* qsz, int64_t n, int64_t m,
+                                int bits, int64_t group, const void* x, int x_dtype,
+                                int64_t tokens, int64_t ldx, float* y, int64_t ldy, int accumulate,
+                                int prologue, const float* prologue_w, float eps, void* workspace,
+                                int64_t workspace_bytes, const qigen_gemv_chain_opts* opts,
+                                void* stream) {
+  return gemv_entry(qw, qsz, n, m, bits, group, x, x_dtype, tokens, ldx, y, ldy, accumulate, 0,
+                    prologue, prologue_w, eps, workspace, workspace_bytes, stream, nullptr, opts);
 }
 
 extern "C" int qigen_gemv_tp_push(const qigen_tp_comm* comm, int slot, const uint32_t* qw,

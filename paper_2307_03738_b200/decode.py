@@ -320,6 +320,10 @@ class GpuLinear:
         return self.pw.gemv(x, out=out, accumulate=accumulate, prologue=prologue,
                             norm_weight=norm_weight, eps=eps)
 
+    def chain(self, x, out, **kw):
+        """A GEMV of the dependent decode chain (PanelWeights.chain)."""
+        return self.pw.chain(x, out, **kw)
+
     def push(self, comm: "TpComm", slot: int, x: torch.Tensor, prologue: str | None = None):
         """Row-parallel partial x W into every rank's inbox (qigen_gemv_tp_push)."""
         self.pw.push(comm, slot, x, prologue=prologue)
@@ -417,6 +421,14 @@ class LlamaTP:
         # off by default: neutral on 7B, slower on 65B (same-box A/B, bench.py)
         self.fold_qkv_norm = (batch <= 2 and backend is GpuBackend
                               and os.environ.get("QIGEN_FOLD_QKV_NORM", "0") == "1")
+        # one GPU, 1-2 tokens: o_proj and down write the activation digits of the
+        # next RMSNorm'd GEMV (gate|up, next layer's QKV) in their epilogue, the
+        # norm folded (1 / rms in the consumer's epilogue), so those GEMVs need no
+        # prep kernel or prologue (qigen_gemv_chain).  Measured (same box, B200,
+        # 7B TP1 B=1): 625 vs 591 tok/s; letting gate|up also write SwiGLU digits
+        # for down (256-column CTAs) measured slower (554) and was dropped.
+        self.chained = (self.tp.world == 1 and backend is GpuBackend and not self.fold_qkv_norm
+                        and batch <= 2 and os.environ.get("QIGEN_CHAIN", "1") == "1")
         self.layers = []
         for li in range(cfg.n_layers):
             base = 100 * li
@@ -468,6 +480,11 @@ class LlamaTP:
                 del g
         self.attn_ws = backend.attention_workspace(batch, self.nh, hd, max_ctx, self.dev)
         self.keep_logits = keep_logits
+        if self.chained:
+            from .runtime import digits_buffer, ss_count
+            self.dig = [digits_buffer(d, batch, self.dev) for _ in range(2)]
+            self.ssc = ss_count(d)
+            self.ss = [torch.zeros(batch * self.ssc, device=self.dev) for _ in range(2)]
         self.fused_head = hasattr(backend, "lm_head") and self.dev.type == "cuda" and batch <= 8
         if self.fused_head:
             self.head_ws = backend.lm_head_workspace(self.v1 - self.v0, d, batch, self.dev)
@@ -525,6 +542,9 @@ class LlamaTP:
         scale = 1.0 / math.sqrt(hd)
         att = torch.empty((B, self.nh * hd), dtype=torch.float32, device=self.dev)
         for li, lay in enumerate(self.layers):
+            if self.chained:
+                yield from self._layer_chained(li, lay, h, att, cos, sin, pos, scale)
+                continue
             if self.fold_qkv_norm:
                 qkv = lay["qkv"](h, prologue="rmsnorm_folded", eps=cfg.norm_eps)
             else:
@@ -552,6 +572,34 @@ class LlamaTP:
         self.tp.argmax_post(mx, ix, logits if self.keep_logits else None, self.v_sizes)
         yield
         self.next_tokens, self.last_logits = self.tp.argmax_collect()
+
+    def _layer_chained(self, li, lay, h, att, cos, sin, pos, scale):
+        """One layer on one GPU without activation prep kernels: o_proj and down
+        write the activation digits of gate|up and of the next layer's QKV
+        (times that GEMV's RMSNorm weight) plus their sums of squares, the
+        consumers apply 1 / rms in their epilogue."""
+        cfg, B, hd = self.cfg, self.B, self.cfg.head_dim
+        eps, g = cfg.norm_eps, cfg.group
+        qkv = torch.empty((B, 3 * self.nh * hd), dtype=torch.float32, device=self.dev)
+        if li == 0:  # the embedding has no producer GEMV
+            lay["qkv"](h, out=qkv, prologue="rmsnorm", norm_weight=lay["n1"], eps=eps)
+        else:
+            lay["qkv"].chain(None, qkv, tokens=B, digits_in=self.dig[1], ss_in=self.ss[1],
+                             ss_count=self.ssc, eps=eps)
+        self.backend.attention(qkv, cos, sin, self.k_cache[li], self.v_cache[li], pos, scale,
+                               att, self.attn_ws)
+        lay["o"].chain(att, h, tokens=B, accumulate=True, digits_out=self.dig[0],
+                       out_scale=lay["n2"], out_group=g, ss_out=self.ss[0])
+        gu = torch.empty((B, 2 * self.nf), dtype=torch.float32, device=self.dev)
+        lay["gu"].chain(None, gu, tokens=B, digits_in=self.dig[0], ss_in=self.ss[0],
+                        ss_count=self.ssc, eps=eps)
+        last = li + 1 == len(self.layers)
+        lay["down"].chain(gu, h, tokens=B, accumulate=True, prologue="swiglu",
+                          digits_out=None if last else self.dig[1],
+                          out_scale=None if last else self.layers[li + 1]["n1"], out_group=g,
+                          ss_out=None if last else self.ss[1])
+        return
+        yield  # (generator)
 
     def _row_parallel(self, lin, x: torch.Tensor, h: torch.Tensor, prologue, slot: int,
                       layer: int):

@@ -227,6 +227,41 @@ class PanelWeights:
         return out.reshape(self.m) if squeeze else out
 
 
+    def chain(self, x: torch.Tensor | None, out: torch.Tensor, *, tokens: int,
+              accumulate: bool = False, prologue: str | None = None,
+              norm_weight: torch.Tensor | None = None, eps: float = 1e-5,
+              digits_in: torch.Tensor | None = None, ss_in: torch.Tensor | None = None,
+              ss_count: int = 0, digits_out: torch.Tensor | None = None,
+              out_scale: torch.Tensor | None = None, out_group: int | None = None,
+              ss_out: torch.Tensor | None = None) -> torch.Tensor:
+        """One GEMV of a dependent decode chain (qigen_gemv_chain): the consumer
+        side reads the activation digits a producer's epilogue wrote
+        (``digits_in``, with the producer's sums of squares ``ss_in`` folding an
+        RMSNorm into the epilogue); the producer side also writes its final
+        output (after the residual add) as the next GEMV's digits
+        (``digits_out``, times ``out_scale``) and ``ss_out``."""
+        from ._lib import ChainOpts
+        import ctypes
+        mode = {None: 0, "rmsnorm": 1, "swiglu": 2}[prologue]
+        if digits_in is None:
+            x2 = x.reshape(tokens, -1)
+            xp, xd, ldx = x2.data_ptr(), _DTYPES[x2.dtype], x2.stride(0)
+        else:
+            xp, xd, ldx = None, F32, self.n
+        o = ChainOpts(None if digits_in is None else digits_in.data_ptr(),
+                      None if ss_in is None else ss_in.data_ptr(), int(ss_count), float(eps),
+                      None if digits_out is None else digits_out.data_ptr(),
+                      None if out_scale is None else out_scale.data_ptr(),
+                      0 if out_group is None else int(out_group),
+                      None if ss_out is None else ss_out.data_ptr())
+        ws = self._workspace(min(tokens, MAX_GEMV_TOKENS), out.device)
+        y2 = out.reshape(tokens, self.m)
+        call("qigen_gemv_chain", self.qw.data_ptr(), self.qsz.data_ptr(), self.n, self.m,
+             self.bits, self.group_code, xp, xd, tokens, ldx, y2.data_ptr(), y2.stride(0),
+             int(accumulate), mode, norm_weight.data_ptr() if mode == 1 else None, float(eps),
+             ws.data_ptr(), ws.numel(), ctypes.byref(o), _dev.stream_handle())
+        return out
+
     def push(self, comm, slot: int, x: torch.Tensor, *, prologue: str | None = None,
              norm_weight: torch.Tensor | None = None, eps: float = 1e-5) -> None:
         """Row-parallel partial x W of a tensor-parallel rank, stored by the GEMV
@@ -247,6 +282,17 @@ class PanelWeights:
 
 
 X_READY = 2  # QIGEN_GEMV_X_READY (include/qigen_b200.h)
+
+
+def digits_buffer(n: int, tokens: int, device) -> torch.Tensor:
+    """Zero-filled prepared-digit buffer for a GEMV with K = n (qigen_gemv_chain)."""
+    return torch.zeros(int(lib().qigen_gemv_workspace_size(n, tokens)), dtype=torch.uint8,
+                       device=device)
+
+
+def ss_count(m: int) -> int:
+    """Per-CTA sums of squares a chain producer with m outputs writes per token."""
+    return int(lib().qigen_gemv_ss_count(m))
 
 
 class GemvGroup:

@@ -258,3 +258,26 @@ def test_emulated_tp_push_matches_tp1(world, cfg):
     for m in models:
         assert torch.allclose(m.k_cache[:, :, :, ctx].float(),
                               ref.k_cache[:, :, m.h0:m.h1, ctx].float(), atol=2e-3, rtol=2e-3)
+
+
+@pytest.mark.gpu
+def test_chained_decode_matches_unchained():
+    """The one-GPU decode step with the digit-epilogue chain (no prep kernels)
+    against the same model with separate RMSNorm prologues: same tokens,
+    logits within 1e-4 of max|logit|, over two steps."""
+    import os
+    cfg = D.LlamaConfig(n_layers=3, d_model=1024, n_heads=8, head_dim=128, ffn=2816, vocab=2000,
+                        bits=4, group=64)
+    for B in (1, 2):
+        os.environ["QIGEN_CHAIN"] = "0"
+        ref = D.LlamaTP(cfg, batch=B, max_ctx=40, seed=3, device="cuda")
+        os.environ["QIGEN_CHAIN"] = "1"
+        m = D.LlamaTP(cfg, batch=B, max_ctx=40, seed=3, device="cuda")
+        assert m.chained and not ref.chained
+        tok = torch.arange(B, device="cuda") * 131 + 7
+        for pos in (30, 31):
+            t1, t2 = ref.step(tok, pos), m.step(tok, pos)
+            l1, l2 = ref.last_logits.double(), m.last_logits.double()
+            assert ((l2 - l1).abs().max() / (1 + l1.abs().max())).item() < 1e-4
+            assert torch.equal(t1, t2)
+            tok = t1

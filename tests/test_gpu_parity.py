@@ -698,3 +698,41 @@ def test_qgemv_batch_device_inputs(q):
     ys = q.qgemv_batch(pms, xs)
     for y, r in zip(ys, refs):
         assert y.is_cuda and rel_err(y.cpu().numpy(), r) <= TOL
+
+
+@pytest.mark.parametrize("gc", [32, 64, 128, None])
+@pytest.mark.parametrize("tokens", [1, 3])
+def test_gemv_chain_digit_epilogue(q, gc, tokens):
+    """qigen_gemv_chain: a producer GEMV (residual add) writes its output as the
+    consumer's activation digits (times the consumer's RMSNorm weight) plus
+    per-CTA sums of squares; the consumer reads the digits and applies 1 / rms
+    in its epilogue.  Against the same two steps done separately (RMSNorm in
+    torch float64, then the oracle-checked GEMV)."""
+    from paper_2307_03738_b200.runtime import digits_buffer, ss_count
+    K1, d, M2 = 2048, 1280, 768
+    rng = np.random.default_rng(7 + tokens + (gc or 0))
+    P = q.PanelWeights.from_float(rng.normal(0, 0.02, (K1, d)).astype(np.float32),
+                                  q.QuantConfig(4, 128))
+    cmc = q.quantize_matrix(rng.normal(0, 0.02, (d, M2)).astype(np.float32), q.QuantConfig(3, gc))
+    C = q.PanelWeights.from_codes(cmc)
+    codes, s, z = cmc.numpy()
+    x = torch.from_numpy(rng.normal(0, 1, (tokens, K1)).astype(np.float32)).cuda()
+    h = torch.from_numpy(rng.normal(0, 1, (tokens, d)).astype(np.float32)).cuda()
+    w = torch.from_numpy(rng.uniform(0.5, 1.5, d).astype(np.float32)).cuda()
+    h_ref = h + P.gemv(x)
+    dig = digits_buffer(d, tokens, "cuda")
+    ssc = ss_count(d)
+    ss = torch.zeros(tokens * ssc, device="cuda")
+    for _ in range(2):  # buffers are reusable
+        hh = h.clone()
+        P.chain(x, hh, tokens=tokens, accumulate=True, digits_out=dig, out_scale=w, out_group=gc,
+                ss_out=ss)
+        y = torch.empty(tokens, M2, device="cuda")
+        C.chain(None, y, tokens=tokens, digits_in=dig, ss_in=ss, ss_count=ssc, eps=1e-5)
+        torch.cuda.synchronize()
+        assert torch.allclose(hh, h_ref, rtol=0, atol=1e-5)
+        hd = hh.double().cpu().numpy()
+        xn = hd / np.sqrt((hd ** 2).mean(-1, keepdims=True) + 1e-5) * w.double().cpu().numpy()
+        ref = orc.qgemv_reference(codes, s, z, xn)
+        assert rel_err(y.cpu().numpy(), ref) <= TOL, (gc, tokens, rel_err(y.cpu().numpy(), ref))
+        assert np.allclose(ss.view(tokens, ssc).sum(1).cpu().numpy(), (hd ** 2).sum(1), rtol=1e-5)
