@@ -411,6 +411,13 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
       for (int i = threadIdx.x; i < C; i += T)
         ep_w[i] = a.dout_w && c0 + i < a.m ? __ldg(a.dout_w + c0 + i) : 1.f;
   }
+  if (a.ss_in && ys == 0 && threadIdx.x < M) {
+    // RMSNorm of x folded into the epilogue: 1 / rms from the producer's per-CTA
+    // sums of squares, fixed order (read now: no dependent load at the end)
+    float ss = 0.f;
+    for (int c = 0; c < a.ss_n; ++c) ss += a.ss_in[threadIdx.x * a.ss_n + c];
+    ((float*)(smem + L.inv))[threadIdx.x] = rsqrtf(ss / (float)a.n + a.eps);
+  }
 
   // ---- 3. activation digits for this chunk into shared memory ----------------
   if (a.dig) {
@@ -639,15 +646,6 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     }
     __syncthreads();
   }
-  if (a.ss_in && rank == 0) {  // RMSNorm of x folded: 1 / rms from the producer's sums
-    float* invs = (float*)(smem + L.inv);
-    if (threadIdx.x < M) {
-      float ss = 0.f;
-      for (int c = 0; c < a.ss_n; ++c) ss += a.ss_in[threadIdx.x * a.ss_n + c];
-      invs[threadIdx.x] = rsqrtf(ss / (float)a.n + a.eps);
-    }
-    __syncthreads();
-  }
   if (early_x && rank == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before y
   trace_point(a, 7);
 #pragma unroll
@@ -689,7 +687,9 @@ __global__ void __launch_bounds__(WPC * 32, 2) gemv_kernel(const GemvArgs a) {
     // next GEMV's K: digitise them in the act_prep layout (item it = 4 rows:
     // step it >> 3, sub-item it & 7), dout_ipu items per exponent unit, and
     // publish this CTA's sum of squares per token.
+    trace_point(a, 12);
     __syncthreads();
+    trace_point(a, 13);
     const float* ev = ep_fin;
     for (int tk = warp; tk < M; tk += WPC) {  // (WPC = 8: one warp-wide unit set per token)
       const int it_l = lane;

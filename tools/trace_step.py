@@ -98,9 +98,14 @@ for key, t in rows:
                 f"exit {ex.min():7.2f}-{ex.max():7.2f}")
         last = ex.max()
     else:
+        own = t[:, 7] > 0  # the CTAs that write y (cluster rank 0)
         line = (f"{str(key):14s} n={len(t):4d} entry {r[:,0].min():7.2f}-{r[:,0].max():7.2f} "
                 f"wait {r[:,1].min():7.2f}-{r[:,1].max():7.2f} prol {np.median(r[:,2]):7.2f} "
-                f"loop {np.median(r[:,3]):7.2f}/{r[:,3].max():7.2f} exit {r[:,4].min():7.2f}-{r[:,4].max():7.2f}")
+                f"loop {np.median(r[:,3]):7.2f}/{r[:,3].max():7.2f} clw {np.median(r[:,6]):7.2f}/{r[:,6].max():7.2f} "
+                f"red {np.median(r[own,7]):7.2f}/{r[own,7].max():7.2f} "
+                + (f"dsync {np.median(r[own,12]):7.2f}/{r[own,12].max():7.2f}->{np.median(r[own,13]):7.2f}/{r[own,13].max():7.2f} "
+                   if (t[own, 12] > 0).any() else "")
+                + f"exit {r[:,4].min():7.2f}-{r[:,4].max():7.2f}")
         last = r[:, 4].max()
     gap = "" if prev_exit is None else f"  gap {r[:,0].min() - prev_exit:5.2f}"
     print(line + gap)
