@@ -302,6 +302,16 @@ int qigen_lm_head(const float* h, const float* norm_w, float eps, const void* w_
                   float* out_max, int64_t* out_idx, void* workspace, int64_t workspace_bytes,
                   void* stream);
 
+/* qigen_attn_decode whose heads also write their outputs as the o_proj GEMV's
+ * prepared activation digits (qigen_gemv_chain_opts.x_digits of a GEMV with K
+ * = heads * head_dim, `batch` tokens, group size o_group >= 64): the o_proj
+ * GEMV then needs no prologue.  head_dim 128. */
+int qigen_attn_decode_chain(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
+                            const float* cos_pos, const float* sin_pos, void* k_cache,
+                            void* v_cache, int64_t ctx, int64_t pos, float scale, float* out,
+                            void* workspace, int64_t workspace_bytes, void* o_digits,
+                            int64_t o_group, void* stream);
+
 /* Small-batch quantized GEMM on the tcgen05 tensor cores (north_star (c)):
  * weights dequantized to fp16 (w = s (c - z)) in shared memory, activations
  * converted to fp16, f32 accumulation in TMEM.  4-bit, group 32..256 (dividing

@@ -94,6 +94,8 @@ SIGNATURES = {
     "qigen_lm_head_workspace_size": (_I64, [_I64, _I64, _I64]),
     "qigen_lm_head": (_I32, [_P, _P, ctypes.c_float, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                              _I64, _P]),
+    "qigen_attn_decode_chain": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64,
+                                       ctypes.c_float, _P, _P, _I64, _P, _I64, _P]),
     "qigen_gemm_tc_workspace_size": (_I64, [_I64, _I64]),
     "qigen_gemm_tc": (_I32, [_P, _P, _I64, _I64, _I32, _I64, _P, _I32, _I64, _I64, _P, _I64, _I32,
                              _I32, _P, _I64, _P]),

@@ -101,6 +101,11 @@ struct AttnArgs {
   int B, H, ctx, pos, nsplit, chunk;
   float scale;
   unsigned long long* trace;  // optional per-CTA %globaltimer: entry, after wait, exit
+  // decode chain: the head's output also written as the o_proj GEMV's prepared
+  // activation digits (qigen_gemv_chain layout: K = H * HD, dout_ipu items per
+  // exponent unit, dout_tp padded tokens, dout_ks supersteps of K)
+  unsigned char* dout;
+  int dout_tp, dout_ks, dout_ipu;
 };
 
 __device__ __forceinline__ void attn_trace(const AttnArgs& a, int i) {
@@ -287,6 +292,25 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const AttnArg
     float acc = 0.f;
     for (int s = 0; s < a.nsplit; ++s) acc += ps[s] * inbox[s * (HD + 2) + d];
     a.out[(size_t)b * a.H * HD + h * HD + d] = acc * inv;
+    if (a.dout) qs[d] = acc * inv;  // (q is no longer needed)
+  }
+  if constexpr (HD == 128) {
+    if (a.dout) {
+      // this head's 128 outputs are rows [h HD, (h + 1) HD) of o_proj's K: one
+      // warp digitises them (act_prep layout, item = 4 rows)
+      __syncthreads();
+      if (warp == 0) {
+        const int kl = 32 * (lane >> 3) + 16 * ((lane & 7) >> 2) + 4 * (lane & 3);
+        const float v4[4] = {qs[kl], qs[kl + 1], qs[kl + 2], qs[kl + 3]};
+        const Digits d = a.dout_ipu == 32 ? digitize<32>(v4, 0xffffffffu)
+                                          : digitize<16>(v4, 0xffffu << (lane & 16));
+        const int it = h * (HD / 4) + lane;
+        store_digits((uint32_t*)a.dout, it >> 3, b, a.dout_tp, it & 7, d);
+        if ((it % a.dout_ipu) == 0)
+          ((float2*)(a.dout + (size_t)a.dout_ks * 8 * a.dout_tp * 128))[(it / a.dout_ipu) * a.dout_tp + b] =
+              make_float2(d.xsum, d.scale);
+      }
+    }
   }
   attn_trace(a, 3);
 }
@@ -314,10 +338,11 @@ extern "C" int64_t qigen_attn_decode_workspace_size(int64_t batch, int64_t heads
   return 0;  // the split partials are combined on chip (cluster shared memory)
 }
 
-extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
-                                 const float* cos_pos, const float* sin_pos, void* k_cache,
-                                 void* v_cache, int64_t ctx, int64_t pos, float scale, float* out,
-                                 void* workspace, int64_t workspace_bytes, void* stream) {
+static int attn_decode_impl(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
+                            const float* cos_pos, const float* sin_pos, void* k_cache,
+                            void* v_cache, int64_t ctx, int64_t pos, float scale, float* out,
+                            void* workspace, int64_t workspace_bytes, void* o_digits,
+                            int64_t o_group, void* stream) {
   (void)workspace; (void)workspace_bytes;
   QIGEN_CHECK_ARG(qkv && cos_pos && sin_pos && k_cache && v_cache && out, QIGEN_ERR_ARG,
                   "null pointer");
@@ -348,6 +373,17 @@ extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads,
   a.scale = scale;
   a.out = out;
   a.trace = g_attn_trace;
+  a.dout = (unsigned char*)o_digits;
+  if (o_digits) {
+    QIGEN_CHECK_ARG(head_dim == 128 && batch <= 16 && (o_group == 64 || o_group == 128 ||
+                                                       o_group == 0 || o_group % 256 == 0),
+                    QIGEN_ERR_UNSUPPORTED,
+                    "attention digit output: head_dim 128, <= 16 tokens, o_proj group >= 64");
+    const int nb = (int)(batch + 1) / 2;
+    a.dout_tp = 2 * (nb <= 1 ? 1 : nb <= 2 ? 2 : nb <= 4 ? 4 : 8);
+    a.dout_ks = (int)supersteps(heads * head_dim);
+    a.dout_ipu = o_group == 64 ? 16 : 32;
+  }
   auto kern = head_dim == 128 ? attn_decode_kernel<128> : attn_decode_kernel<64>;
   static OncePerDevice once;
   const int cst = once.run([]() -> int {
@@ -400,4 +436,23 @@ extern "C" int qigen_rmsnorm_f16(const float* h, const float* w, int64_t rows, i
                                                                        (__half*)out);
   QIGEN_CUDA_RET(cudaGetLastError());
   return QIGEN_OK;
+}
+
+extern "C" int qigen_attn_decode(const float* qkv, int64_t batch, int64_t heads, int64_t head_dim,
+                                 const float* cos_pos, const float* sin_pos, void* k_cache,
+                                 void* v_cache, int64_t ctx, int64_t pos, float scale, float* out,
+                                 void* workspace, int64_t workspace_bytes, void* stream) {
+  return attn_decode_impl(qkv, batch, heads, head_dim, cos_pos, sin_pos, k_cache, v_cache, ctx,
+                          pos, scale, out, workspace, workspace_bytes, nullptr, 0, stream);
+}
+
+extern "C" int qigen_attn_decode_chain(const float* qkv, int64_t batch, int64_t heads,
+                                       int64_t head_dim, const float* cos_pos,
+                                       const float* sin_pos, void* k_cache, void* v_cache,
+                                       int64_t ctx, int64_t pos, float scale, float* out,
+                                       void* workspace, int64_t workspace_bytes, void* o_digits,
+                                       int64_t o_group, void* stream) {
+  QIGEN_CHECK_ARG(o_digits, QIGEN_ERR_ARG, "null digit buffer");
+  return attn_decode_impl(qkv, batch, heads, head_dim, cos_pos, sin_pos, k_cache, v_cache, ctx,
+                          pos, scale, out, workspace, workspace_bytes, o_digits, o_group, stream);
 }

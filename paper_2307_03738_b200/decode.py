@@ -346,12 +346,21 @@ class GpuBackend:
              _dev.stream_handle())
 
     @staticmethod
-    def attention(qkv, cos, sin, k_cache, v_cache, pos, scale, out, workspace):
-        """RoPE + KV append + split-KV attention in one kernel (decode_ops.cu)."""
+    def attention(qkv, cos, sin, k_cache, v_cache, pos, scale, out, workspace, o_digits=None,
+                  o_group=None):
+        """RoPE + KV append + split-KV attention in one kernel (decode_ops.cu);
+        with ``o_digits`` the heads also write the o_proj GEMV's activation
+        digits (qigen_attn_decode_chain)."""
         B, H, ctx, hd = k_cache.shape
-        call("qigen_attn_decode", qkv.data_ptr(), B, H, hd, cos.data_ptr(), sin.data_ptr(),
-             k_cache.data_ptr(), v_cache.data_ptr(), ctx, pos, float(scale), out.data_ptr(),
-             workspace.data_ptr(), workspace.numel(), _dev.stream_handle())
+        if o_digits is None:
+            call("qigen_attn_decode", qkv.data_ptr(), B, H, hd, cos.data_ptr(), sin.data_ptr(),
+                 k_cache.data_ptr(), v_cache.data_ptr(), ctx, pos, float(scale), out.data_ptr(),
+                 workspace.data_ptr(), workspace.numel(), _dev.stream_handle())
+        else:
+            call("qigen_attn_decode_chain", qkv.data_ptr(), B, H, hd, cos.data_ptr(),
+                 sin.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), ctx, pos, float(scale),
+                 out.data_ptr(), workspace.data_ptr(), workspace.numel(), o_digits.data_ptr(),
+                 0 if o_group is None else int(o_group), _dev.stream_handle())
 
     @staticmethod
     def attention_workspace(B, H, hd, ctx, device):
@@ -483,6 +492,9 @@ class LlamaTP:
         if self.chained:
             from .runtime import digits_buffer, ss_count
             self.dig = [digits_buffer(d, batch, self.dev) for _ in range(2)]
+            # attention -> o_proj digits (head_dim 128, o_proj group >= 64)
+            self.att_dig = (digits_buffer(self.nh * hd, batch, self.dev)
+                            if hd == 128 and (cfg.group is None or cfg.group >= 64) else None)
             self.ssc = ss_count(d)
             self.ss = [torch.zeros(batch * self.ssc, device=self.dev) for _ in range(2)]
         self.fused_head = hasattr(backend, "lm_head") and self.dev.type == "cuda" and batch <= 8
@@ -587,9 +599,10 @@ class LlamaTP:
             lay["qkv"].chain(None, qkv, tokens=B, digits_in=self.dig[1], ss_in=self.ss[1],
                              ss_count=self.ssc, eps=eps)
         self.backend.attention(qkv, cos, sin, self.k_cache[li], self.v_cache[li], pos, scale,
-                               att, self.attn_ws)
-        lay["o"].chain(att, h, tokens=B, accumulate=True, digits_out=self.dig[0],
-                       out_scale=lay["n2"], out_group=g, ss_out=self.ss[0])
+                               att, self.attn_ws, o_digits=self.att_dig, o_group=g)
+        lay["o"].chain(att, h, tokens=B, accumulate=True, digits_in=self.att_dig,
+                       digits_out=self.dig[0], out_scale=lay["n2"], out_group=g,
+                       ss_out=self.ss[0])
         gu = torch.empty((B, 2 * self.nf), dtype=torch.float32, device=self.dev)
         lay["gu"].chain(None, gu, tokens=B, digits_in=self.dig[0], ss_in=self.ss[0],
                         ss_count=self.ssc, eps=eps)

@@ -48,11 +48,11 @@ D.GpuLinear.chain = wrap(D.GpuLinear.chain)
 att0 = D.GpuBackend.attention
 
 
-def attn(*a):
+def attn(*a, **kw):
     key = (state["i"] // 4, "attn")
     Lb.qigen_debug_attn_trace(buf(key, 4).data_ptr())
     try:
-        att0(*a)
+        att0(*a, **kw)
     finally:
         Lb.qigen_debug_attn_trace(None)
 
