@@ -359,6 +359,53 @@ int qigen_debug_attn_trace(void* buf);
 /* Tuning aid: cap on the position splits (cluster size, <= 16) per head of the decode attention. */
 int qigen_debug_attn_splits(int n);
 
+/* ---- persistent decode stack (csrc/decode_stack.cu) --------------------------- */
+
+/* All layers of a batch-1 LLaMA-architecture decode step on one GPU as ONE
+ * persistent launch (one CTA per SM; the layers' quantized linears and the
+ * attention are phases separated by grid barriers, weights stream through
+ * per-warp rings that never drain between phases).  Consumer of the quantized
+ * GEMV; no reference counterpart (the reference has no model path),
+ * the arithmetic of each linear is that of qigen_gemv (kernelgen.py:227-240).
+ * Per layer: RMSNorm -> fused QKV -> RoPE + KV append + attention over
+ * positions 0..pos -> o_proj + residual -> RMSNorm -> fused gate|up -> SwiGLU ->
+ * down_proj + residual.  Deterministic. */
+typedef struct qigen_stack_layer {
+  const void* qw[4];    /* panel words of W_qkv [d, 3d] (q | k | v heads), W_o [d, d],
+                           W_gate|up [d, 2 ffn], W_down [ffn, d] */
+  const void* qsz[4];   /* their (s, z) */
+  const float* norm1;   /* RMSNorm weight before QKV [d] */
+  const float* norm2;   /* RMSNorm weight before gate|up [d] */
+  void* k_cache;        /* f16 [heads][ctx][128]; row `pos` is appended by the step */
+  void* v_cache;
+} qigen_stack_layer;
+typedef struct qigen_stack_desc {
+  int32_t layers, d_model, heads, head_dim, ffn, bits;
+  int64_t group_size;   /* 32, 64 or 128 */
+  int64_t ctx;          /* rows of the KV caches */
+  float eps;            /* RMSNorm epsilon */
+} qigen_stack_desc;
+typedef struct qigen_decode_stack qigen_decode_stack;
+/* QIGEN_ERR_UNSUPPORTED for shapes outside the kernel's limits (head_dim != 128,
+ * other group sizes, ...): callers fall back to the per-op chain. */
+int qigen_decode_stack_create(const qigen_stack_desc* desc, const qigen_stack_layer* layers,
+                              qigen_decode_stack** out);
+/* h_in: the embedded token f32 [d]; h_out: the residual after the last layer
+ * f32 [d] (input of the final RMSNorm + LM head); cosv / sinv: RoPE factors of
+ * `pos` f32 [64]; scale: 1 / sqrt(head_dim).  Stream-ordered, graph-capturable.
+ * One run at a time per handle. */
+int qigen_decode_stack_run(const qigen_decode_stack* s, const float* h_in, float* h_out,
+                           const float* cosv, const float* sinv, int64_t pos, float scale,
+                           void* stream);
+/* Synchronous: non-zero *out if a wait inside the last runs timed out (bit 0: grid
+ * barrier, bit 1: weight stage); re-arms the handle. */
+int qigen_decode_stack_error(const qigen_decode_stack* s, int* out);
+int qigen_decode_stack_info(const qigen_decode_stack* s, int* grid, int* depth, int* smem_bytes);
+int qigen_decode_stack_destroy(qigen_decode_stack* s);
+/* Tuning aid (per calling thread, read at create): supersteps per weight stage
+ * (1 or 2) and the cap on ring stages per warp. */
+int qigen_debug_stack_tuning(int sss, int depth);
+
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
 
 typedef struct qigen_weights qigen_weights;

@@ -37,6 +37,19 @@ class ChainOpts(ctypes.Structure):
                 ("y_digits", _P), ("out_scale", _P), ("out_group", _I64), ("ss_out", _P)]
 
 
+class StackLayer(ctypes.Structure):
+    """qigen_stack_layer (include/qigen_b200.h)."""
+    _fields_ = [("qw", _P * 4), ("qsz", _P * 4), ("norm1", _P), ("norm2", _P),
+                ("k_cache", _P), ("v_cache", _P)]
+
+
+class StackDesc(ctypes.Structure):
+    """qigen_stack_desc (include/qigen_b200.h)."""
+    _fields_ = [("layers", _I32), ("d_model", _I32), ("heads", _I32), ("head_dim", _I32),
+                ("ffn", _I32), ("bits", _I32), ("group_size", _I64), ("ctx", _I64),
+                ("eps", ctypes.c_float)]
+
+
 class GemvDesc(ctypes.Structure):
     """qigen_gemv_desc (include/qigen_b200.h)."""
     _fields_ = [("qw", _P), ("qsz", _P), ("n", _I64), ("m", _I64), ("bits", _I32),
@@ -109,6 +122,13 @@ SIGNATURES = {
     "qigen_debug_group_mode": (_I32, [_I32]),
     "qigen_debug_attn_trace": (_I32, [_P]),
     "qigen_debug_attn_splits": (_I32, [_I32]),
+    "qigen_decode_stack_create": (_I32, [_P, _P, ctypes.POINTER(_P)]),
+    "qigen_decode_stack_run": (_I32, [_P, _P, _P, _P, _P, _I64, ctypes.c_float, _P]),
+    "qigen_decode_stack_error": (_I32, [_P, ctypes.POINTER(_I32)]),
+    "qigen_decode_stack_info": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32),
+                                       ctypes.POINTER(_I32)]),
+    "qigen_decode_stack_destroy": (_I32, [_P]),
+    "qigen_debug_stack_tuning": (_I32, [_I32, _I32]),
     "qigen_weights_create": (_I32, [_P, _I32, _I64, _I64, _I32, _I64, _I64, _I64, _P, _I64,
                                     _P, _P, _P, ctypes.POINTER(_P)]),
     "qigen_weights_destroy": (_I32, [_P]),

@@ -1,0 +1,967 @@
+// Persistent decode stack: every layer of a LLaMA-architecture decode step
+// (batch 1, one GPU) as ONE launch.
+//
+// The per-op chain of the decode driver (decode.py) is latency-bound: each of
+// the five kernels of a layer pays its launch boundary, its activation
+// prologue and its split-K tail on the critical path.  Here one
+// CTA per SM stays resident for the whole step:
+//   * the four quantized linears of every layer (fused QKV, o_proj, fused
+//     gate|up, down_proj; same arithmetic as gemv.cu / gemv_grouped.cu: the
+//     reference factorisation kernelgen.py:227-240 with exact IMMA partials)
+//     and the attention in between are PHASES separated by a grid barrier (one
+//     global counter, release/acquire);
+//   * a phase's work is its (panel, superstep) units in panel-major order,
+//     cut into equal contiguous ranges, one per warp of the grid (148 x 16):
+//     every warp streams its range through its own ring of TMA bulk-copy
+//     stages.  The schedule is static, so a warp's issue cursor simply runs
+//     ahead into the NEXT phases (and layers): weights keep streaming from HBM
+//     while the CTA sits in a barrier or digitises activations, and the rings
+//     never drain;
+//   * a warp's partial sums of a panel are reduced inside the CTA in warp
+//     order and stored as one partial per (CTA, panel) ("slot"); the consumer
+//     of the vector adds the slots in CTA order.  No atomics: deterministic;
+//   * the consumer side of each phase ("prologue") is computed redundantly by
+//     every CTA straight into shared memory: residual add, RMSNorm weight,
+//     SwiGLU or the attention combine, then the fixed-point digit records of
+//     the whole K range (1152 B per 256 rows).  The 1/rms of an RMSNorm is
+//     applied to the GEMV's OUTPUT by its consumer (the GEMV is linear);
+//   * attention: each head is split over cph CTAs by position; a warp keeps an
+//     online-softmax state over its positions, the CTA combines its warps and
+//     stores one partial per (head, chunk); the o_proj prologue combines them.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+#include "gemv_common.cuh"
+
+namespace qigen {
+
+extern thread_local unsigned long long* g_trace;  // gemv.cu (qigen_debug_trace)
+
+namespace {
+
+constexpr int kSWarps = 16;
+constexpr int kSThreads = kSWarps * 32;
+constexpr int kSRecDig = 1024;              // digit bytes per superstep record (1 token)
+constexpr int kSRec = kSRecDig + 8 * 16;    // + up to 8 units x {A, B, scale, 0}
+constexpr int kMaxSeg = 4;                  // panel segments per warp and phase
+constexpr int kMaxSlot = 2;                 // partials per output column (grid <= panels)
+constexpr int kAttRow = 132;                // floats per attention partial: acc[128], m, l, pad
+constexpr int kHD = 128;                    // head dimension
+constexpr int kMaxCph = 4;                  // position chunks (CTAs) per head
+constexpr int kAttScratch = (4 * kHD + kSWarps * kAttRow) * 4;
+constexpr int kLtab = 12;                   // pointers per layer in the shared-memory table
+constexpr int kCrow = 34;                   // per phase: lo[17], first panel[16], panel count
+constexpr int kCtab = 4 * kCrow;
+
+struct SLayer {          // device table entry
+  const char* qw[4];     // qkv, o, gate|up, down: panel words
+  const char* qsz[4];    // their (s, z)
+  const float* n1;
+  const float* n2;       // RMSNorm weights
+  __half* kc;
+  __half* vc;            // [H][ctx][128]
+};
+
+struct SPlan {
+  const SLayer* layers;
+  int L, d, H, ffn, ctx, cph, G;
+  uint32_t P[4], S[4], T[4];   // panels, supersteps, units of the four GEMV phases
+  uint32_t pstride[4];         // floats per partial slot (P * 16)
+  float* part[4];              // [slots][P * 16]
+  float* attp;                 // [H][cph][kAttRow]
+  float* hx;                   // residual after o_proj (h')
+  float* hy;                   // residual at layer entry (h)
+  const uint32_t* ctab;        // [G][kCtab]: per CTA and phase, lo[17] | first panel[16] | panels
+  const uint32_t* two;         // bit p of phase ph (word offset two_off[ph]): panel spans two CTAs
+  uint32_t two_off[4], two_words;
+  uint32_t own_q;              // residual items (4 floats) each CTA stores
+  unsigned int* bar;           // [0] barrier counter, [1] error word, [2] exit counter
+  const float* h_in;
+  float* h_out;
+  const float* cosv;
+  const float* sinv;
+  int pos;
+  float scale, eps;
+  int depth, sss;              // ring stages per warp, supersteps per stage
+  uint32_t slot_bytes, xrec_bytes;
+  unsigned long long* trace;   // optional: per barrier and CTA (arrive, pass) in ns
+};
+
+__device__ __forceinline__ void imma_z(int (&c)[4], const uint32_t (&a)[4], uint2 b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};"
+      : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y), "r"(0));
+}
+
+// One 256-row superstep of one panel against the single token's digit record
+// (gemv_grouped.cu group_superstep with a one-token record: the n8 columns 4-7
+// repeat the token's digits and are ignored).
+template <int BITS, int GPS>
+__device__ __forceinline__ void stack_superstep(const uint4 (&w)[BITS], const float2* szs,
+                                                const unsigned char* rec, float (&yv)[2]) {
+  constexpr int UPS = GPS > 2 ? GPS : 2;
+  constexpr int SPU = 8 / UPS;
+  const int lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
+  const uint2* bs = (const uint2*)rec + (gq & 3) * 4 + t;
+  const float2* ab = (const float2*)(rec + kSRecDig) + (t & 1);
+  int acc[2][4];
+#pragma unroll
+  for (int sl = 0; sl < 8; ++sl) {
+    uint32_t af[4];
+    extract<BITS>(w, sl, af);
+    if (sl % SPU < 2) imma_z(acc[sl & 1], af, bs[sl * 16]);
+    else imma(acc[sl & 1], af, bs[sl * 16]);
+    if ((sl + 1) % SPU == 0) {
+      const int uj = (sl + 1) / SPU - 1;
+      const int gi = GPS >= UPS ? uj : 0;
+      const float2 sz0 = szs[gi * 16 + gq], sz1 = szs[gi * 16 + gq + 8];
+      const float2 f = ab[uj * 2];
+      constexpr int sh = BITS == 2 ? 4 : 0;  // 2-bit odd steps carry an extra x16
+      int c0, c1, c2, c3;
+      if (SPU == 1) {
+        const int k = sl & 1, shk = k ? sh : 0;
+        c0 = acc[k][0] >> shk; c1 = acc[k][1] >> shk; c2 = acc[k][2] >> shk; c3 = acc[k][3] >> shk;
+      } else {
+        c0 = acc[0][0] + (acc[1][0] >> sh); c1 = acc[0][1] + (acc[1][1] >> sh);
+        c2 = acc[0][2] + (acc[1][2] >> sh); c3 = acc[0][3] + (acc[1][3] >> sh);
+      }
+      const float q0 = (float)(c0 * 256 + c1), q1 = (float)(c2 * 256 + c3);
+      yv[0] = fmaf(sz0.x, fmaf(-sz0.y, f.y, f.x * q0), yv[0]);
+      yv[1] = fmaf(sz1.x, fmaf(-sz1.y, f.y, (f.x * RowScale<BITS>::inv_hi) * q1), yv[1]);
+    }
+  }
+}
+
+// Unit ranges: warp gw of GW owns [lo(gw), lo(gw + 1)) of T units.
+__host__ __device__ __forceinline__ uint32_t lo_of(uint32_t gw, uint32_t T, uint32_t GW) {
+  return (uint32_t)((uint64_t)gw * T / GW);
+}
+// (host guarantees (T + 1) * GW < 2^32)
+__host__ __device__ __forceinline__ uint32_t warp_of(uint32_t u, uint32_t T, uint32_t GW) {
+  return ((u + 1) * GW - 1) / T;
+}
+
+__device__ __forceinline__ float4 ldcg4(const float* p) { return __ldcg((const float4*)p); }
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+
+__device__ __forceinline__ bool mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  for (int i = 0; i < 300; ++i) {  // x 10 ms suspend hint
+    uint32_t done = 0;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "r"(0x989680u)
+        : "memory");
+    if (done) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int BITS, int GPS>
+__global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan pl) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int WB = BITS * 512, ZB = GPS * 128;
+  constexpr int UPS = GPS > 2 ? GPS : 2, IPU = 64 / UPS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t cta = blockIdx.x, G = (uint32_t)pl.G;
+  const int depth = pl.depth, sss = pl.sss;
+  const uint32_t slot_bytes = pl.slot_bytes;
+
+  unsigned char* xrec = smem;                                          // digit records / attention scratch
+  unsigned char* rings = smem + pl.xrec_bytes;                         // [warp][depth][slot]
+  float* wpart = (float*)(rings + (size_t)kSWarps * depth * slot_bytes);  // [warp][kMaxSeg][16]
+  float* red = wpart + kSWarps * kMaxSeg * 16;                         // [32]
+  uint64_t* fullb = (uint64_t*)(red + 32);                             // [warp][depth]
+  const char** ltab = (const char**)(fullb + kSWarps * depth);  // [L][12]: qw[4], qsz[4], n1, n2, kc, vc
+
+  uint32_t* ctab = (uint32_t*)(ltab + pl.L * kLtab);            // this CTA's unit ranges
+  uint32_t* twob = ctab + kCtab;                                // two-CTA panel bits
+
+  static_assert(sizeof(SLayer) == kLtab * sizeof(void*), "layer table entry");
+  for (int i = tid; i < pl.L * kLtab; i += kSThreads)
+    ltab[i] = ((const char* const*)pl.layers)[i];
+  for (int i = tid; i < kCtab; i += kSThreads) ctab[i] = pl.ctab[(size_t)cta * kCtab + i];
+  for (uint32_t i = tid; i < pl.two_words; i += kSThreads) twob[i] = pl.two[i];
+  if (tid == 0) {
+    for (int i = 0; i < kSWarps * depth; ++i) mbar_init(&fullb[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  unsigned char* ring = rings + (size_t)warp * depth * slot_bytes;
+  uint64_t* full = fullb + warp * depth;
+
+  // ---- issue cursor (lane 0): the warp's static stream of weight stages over
+  // all phases of all layers
+  int c_l = 0, c_ph = -1, islot = 0;
+  uint32_t c_u = 0, c_hi = 0, c_segend = 0;
+  bool c_done = false;
+  const char *c_w = nullptr, *c_z = nullptr;
+  auto next_phase = [&]() {
+    for (;;) {
+      if (++c_ph == 4) {
+        c_ph = 0;
+        if (++c_l == pl.L) {
+          c_done = true;
+          return;
+        }
+      }
+      c_u = ctab[c_ph * kCrow + warp];
+      c_hi = ctab[c_ph * kCrow + warp + 1];
+      if (c_hi > c_u) {
+        c_segend = (ctab[c_ph * kCrow + 17 + warp] + 1) * pl.S[c_ph];
+        c_w = ltab[c_l * kLtab + c_ph];
+        c_z = ltab[c_l * kLtab + 4 + c_ph];
+        return;
+      }
+    }
+  };
+  auto issue_one = [&]() {
+    if (c_done) return;
+    const uint32_t nss = min((uint32_t)sss, min(c_hi, c_segend) - c_u);
+    unsigned char* dst = ring + (size_t)islot * slot_bytes;
+    uint64_t* bar = &full[islot];
+    mbar_expect_tx(bar, nss * (WB + ZB));
+    bulk_g2s(dst, c_w + (size_t)c_u * WB, nss * WB, bar);
+    bulk_g2s(dst + sss * WB, c_z + (size_t)c_u * ZB, nss * ZB, bar);
+    if (++islot == depth) islot = 0;
+    c_u += nss;
+    if (c_u == c_hi) next_phase();
+    else if (c_u == c_segend) c_segend += pl.S[c_ph];
+  };
+  if (lane == 0) {
+    next_phase();
+    for (int i = 0; i < depth; ++i) issue_one();
+  }
+  __syncwarp();
+
+  // ---- grid barrier -----------------------------------------------------------
+  unsigned int nbar = 0;
+  auto stamp = [&](int i) {  // trace point i of the phase ending at barrier nbar
+    if (pl.trace && tid == 0) pl.trace[((size_t)nbar * G + cta) * 4 + i] = gtime();
+  };
+  auto grid_arrive = [&]() {
+    __syncthreads();
+    if (tid == 0) {
+      if (pl.trace) pl.trace[((size_t)nbar * G + cta) * 4] = gtime();
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(pl.bar) : "memory");
+    }
+    ++nbar;
+  };
+  auto grid_wait = [&]() {
+    if (tid == 0) {
+      const unsigned int target = nbar * G;
+      const unsigned long long t0 = gtime();
+      unsigned int spins = 0;
+      for (;;) {
+        unsigned int v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pl.bar) : "memory");
+        if (v >= target) break;
+        if ((++spins & 1023u) == 0 && gtime() - t0 > 2000000000ull) {
+          atomicOr(pl.bar + 1, 1u);
+          break;
+        }
+      }
+      if (pl.trace) pl.trace[((size_t)(nbar - 1) * G + cta) * 4 + 1] = gtime();
+    }
+    __syncthreads();
+  };
+
+  // The four columns c .. c + 3 of a phase's output lie in one panel, which one
+  // CTA or two consecutive CTAs covered (the host keeps the grid <= the panel
+  // count): partial slot 0 and, if `two`, slot 1.  Loads are issued
+  // unconditionally (slot 0 twice for a single-CTA panel) so that a thread's
+  // loads of a whole prologue batch are in flight together.
+  auto two_slots = [&](int ph, uint32_t c) {
+    const uint32_t p = c >> 4;
+    return ((twob[pl.two_off[ph] + (p >> 5)] >> (p & 31)) & 1u) != 0u;
+  };
+  struct Slot4 {
+    float4 a, b;
+    bool two;
+  };
+  auto slot_load4 = [&](int ph, uint32_t c) {
+    Slot4 r;
+    r.two = two_slots(ph, c);
+    const float* src = pl.part[ph] + c;
+    r.a = ldcg4(src);
+    r.b = r.two ? ldcg4(src + pl.pstride[ph]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return r;
+  };
+  auto slot_val4 = [](const Slot4& r) {
+    float4 a = r.a;
+    if (r.two) add4(a, r.b);
+    return a;
+  };
+  auto slot_sum1 = [&](int ph, uint32_t c) {  // one column
+    const bool two = two_slots(ph, c);
+    const float a = __ldcg(pl.part[ph] + c);
+    const float b = two ? __ldcg(pl.part[ph] + pl.pstride[ph] + c) : 0.f;
+    return two ? a + b : a;
+  };
+
+  // Digitise a K vector into the shared-memory records: item it = rows 4 it ..
+  // 4 it + 3.  load(it) fetches the item's inputs (addresses clamped into the
+  // vector), finish(it, raw, v) turns them into the four values (zeros beyond
+  // K); UB items per thread are loaded before any is finished.
+  auto digitize_rows = [&](uint32_t S, auto ub_c, auto&& load, auto&& finish) {
+    constexpr int UB = decltype(ub_c)::value;
+    const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
+    const int nit = (int)S * 64;
+    for (int it0 = warp * 32; it0 < nit; it0 += kSThreads * UB) {
+      decltype(load(0)) r[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) r[u] = load(min(it0 + u * kSThreads + lane, nit - 1));
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (it0 + u * kSThreads < nit) {
+          const int it = it0 + u * kSThreads + lane;
+          float v[4];
+          finish(it, r[u], v);
+          const Digits dg = digitize<IPU>(v, umask);
+          unsigned char* rec = xrec + (size_t)(it >> 6) * kSRec;
+          store_digits((uint32_t*)rec, (it >> 3) & 7, 0, 1, it & 7, dg);
+          if ((it % IPU) == 0)
+            ((float4*)(rec + kSRecDig))[(it & 63) / IPU] =
+                make_float4(dg.scale * 65536.f, dg.xsum * dg.scale, dg.scale, 0.f);
+        }
+      }
+    }
+  };
+  // block sum of a per-thread value (ends with a CTA barrier: also publishes
+  // the records written before it)
+  auto block_sum = [&](float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < kSWarps; ++w) s += red[w];
+    return s;
+  };
+
+  // ---- one GEMV phase: consume this warp's unit range ----------------------------
+  int wslot = 0;
+  uint32_t wph = 0;
+  auto gemv_phase = [&](int ph) {
+    const uint32_t S = pl.S[ph];
+    const uint32_t* row = ctab + ph * kCrow;
+    const uint32_t lo = row[warp], hi = row[warp + 1];
+    uint32_t u = lo, p = row[17 + warp];
+    int seg = 0;
+    while (u < hi) {
+      uint32_t s = u - p * S;
+      const uint32_t seg_end = min(hi, (p + 1) * S);
+      float yv[2] = {0.f, 0.f};
+      while (u < seg_end) {
+        const uint32_t nss = min((uint32_t)sss, seg_end - u);
+        if (!mbar_wait_bounded(&full[wslot], wph)) atomicOr(pl.bar + 1, 2u);
+        const unsigned char* stg = ring + (size_t)wslot * slot_bytes;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j < (int)nss) {
+            uint4 w[BITS];
+#pragma unroll
+            for (int v = 0; v < BITS; ++v) w[v] = ((const uint4*)(stg + j * WB))[v * 32 + lane];
+            stack_superstep<BITS, GPS>(w, (const float2*)(stg + sss * WB + j * ZB),
+                                       xrec + (size_t)(s + j) * kSRec, yv);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue_one();
+        }
+        if (++wslot == depth) {
+          wslot = 0;
+          wph ^= 1u;
+        }
+        u += nss;
+        s += nss;
+      }
+      const float v0 = yv[0] + __shfl_xor_sync(0xffffffffu, yv[0], 1);
+      const float v1 = yv[1] + __shfl_xor_sync(0xffffffffu, yv[1], 1);
+      if ((lane & 3) == 0 && seg < kMaxSeg) {
+        wpart[(warp * kMaxSeg + seg) * 16 + (lane >> 2)] = v0;
+        wpart[(warp * kMaxSeg + seg) * 16 + (lane >> 2) + 8] = v1;
+      }
+      ++seg;
+      ++p;
+    }
+    __syncthreads();
+    stamp(3);
+    // the CTA's partial of every panel it touched: its warps' segments in warp order
+    const uint32_t LO = row[0], HI = row[16], pf = row[17], npan = row[33];
+    if ((uint32_t)tid < npan * 16) {
+      const uint32_t pp = pf + tid / 16, col = tid % 16;
+      const uint32_t ua = max(LO, pp * S), ub = min(HI, (pp + 1) * S) - 1;
+      float acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < kSWarps; ++w) {
+        const uint32_t lw = row[w], hw = row[w + 1];
+        if (hw > lw && hw > ua && lw <= ub)
+          acc += wpart[((uint32_t)w * kMaxSeg + (pp - row[17 + w])) * 16 + col];
+      }
+      // slot 1 when the panel started in the previous CTA
+      pl.part[ph][(pp * S < LO ? pl.pstride[ph] : 0u) + pp * 16 + col] = acc;
+    }
+    grid_arrive();
+  };
+
+  // The cached K / V rows this CTA will read in the attention phase of layer l
+  // (written by earlier steps): pulled into L2 while the QKV phase runs.
+  auto prefetch_kv = [&](int l) {
+    const int cph = pl.cph, ngroups = (int)G / cph;
+    const int gi = (int)cta / cph, j = (int)cta % cph;
+    const int npos = pl.pos + 1, Lc = (npos + cph - 1) / cph;
+    const int p0 = j * Lc, p1 = min(min(p0 + Lc, npos), pl.pos);  // cached rows only
+    if (gi >= ngroups || p1 <= p0 || tid >= 2) return;
+    const char* base = ltab[l * kLtab + 10 + tid];
+    for (int hh = gi; hh < pl.H; hh += ngroups) {
+      const char* src = base + ((size_t)hh * pl.ctx + p0) * kHD * 2;
+      const uint32_t bytes = (uint32_t)(p1 - p0) * kHD * 2;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
+  };
+
+  // ---- attention of layer l (reads the QKV partials x rinv) -------------------------
+  auto attention = [&](int l, float rinv) {
+    float* qs = (float*)xrec;       // rotated q (through f16)
+    float* raw = qs + kHD;          // [3][128]: q, k, v of the new token
+    float* wsm = raw + 3 * kHD;     // [warp][kAttRow]
+    __half* const kc = (__half*)ltab[l * kLtab + 10];
+    __half* const vc = (__half*)ltab[l * kLtab + 11];
+    const int cph = pl.cph, ngroups = (int)G / cph;
+    const int gi = (int)cta / cph, j = (int)cta % cph;
+    const int npos = pl.pos + 1, Lc = (npos + cph - 1) / cph;
+    const int p0 = j * Lc, p1 = min(p0 + Lc, npos);
+    const bool mine = pl.pos >= p0 && pl.pos < p1;  // this chunk holds the new token
+    if (gi < ngroups) {
+      for (int hh = gi; hh < pl.H; hh += ngroups) {
+        if (tid < 3 * kHD && (tid < kHD || mine))
+          raw[tid] = slot_sum1(0, (uint32_t)(tid >> 7) * pl.d + (uint32_t)hh * kHD + (tid & 127)) * rinv;
+        __syncthreads();
+        if (tid < kHD / 2) {
+          const int i = tid;
+          const float c = pl.cosv[i], s = pl.sinv[i];
+          // rotate-half with separately rounded products, q / k rounded through
+          // f16 (decode_ops.cu attn_decode_kernel)
+          auto rot_lo = [&](float x0, float x1) { return __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s)); };
+          auto rot_hi = [&](float x0, float x1) { return __fadd_rn(__fmul_rn(x1, c), __fmul_rn(x0, s)); };
+          const float q0 = raw[i], q1 = raw[i + kHD / 2];
+          qs[i] = __half2float(__float2half_rn(rot_lo(q0, q1)));
+          qs[i + kHD / 2] = __half2float(__float2half_rn(rot_hi(q0, q1)));
+          if (mine) {  // append k, v
+            const float k0 = raw[kHD + i], k1 = raw[kHD + i + kHD / 2];
+            const size_t g = ((size_t)hh * pl.ctx + pl.pos) * kHD;
+            kc[g + i] = __float2half_rn(rot_lo(k0, k1));
+            kc[g + i + kHD / 2] = __float2half_rn(rot_hi(k0, k1));
+            vc[g + i] = __float2half_rn(raw[2 * kHD + i]);
+            vc[g + i + kHD / 2] = __float2half_rn(raw[2 * kHD + i + kHD / 2]);
+          }
+        }
+        __syncthreads();
+        const float4 q = *(const float4*)(qs + 4 * lane);
+        float m = -INFINITY, ls = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+        const __half* kb = kc + (size_t)hh * pl.ctx * kHD + 4 * lane;
+        const __half* vb = vc + (size_t)hh * pl.ctx * kHD + 4 * lane;
+        constexpr int NB = 8;
+        for (int pp = p0 + warp; pp < p1; pp += kSWarps * NB) {
+          uint2 kr[NB], vr[NB];
+          float sc[NB];
+#pragma unroll
+          for (int u = 0; u < NB; ++u) {
+            const int pu = min(pp + kSWarps * u, p1 - 1);
+            kr[u] = __ldcg((const uint2*)(kb + (size_t)pu * kHD));
+            vr[u] = __ldcg((const uint2*)(vb + (size_t)pu * kHD));
+          }
+#pragma unroll
+          for (int u = 0; u < NB; ++u) {
+            const float2 k01 = __half22float2(*(const __half2*)&kr[u].x);
+            const float2 k23 = __half22float2(*(const __half2*)&kr[u].y);
+            sc[u] = q.x * k01.x + q.y * k01.y + q.z * k23.x + q.w * k23.y;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < NB; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+          float mb = m;
+#pragma unroll
+          for (int u = 0; u < NB; ++u) {
+            sc[u] = pp + kSWarps * u < p1 ? sc[u] * pl.scale : -INFINITY;
+            mb = fmaxf(mb, sc[u]);
+          }
+          const float corr = m == -INFINITY ? 0.f : __expf(m - mb);
+          ls *= corr;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] *= corr;
+#pragma unroll
+          for (int u = 0; u < NB; ++u) {
+            const float e = __expf(sc[u] - mb);  // 0 for the masked tail
+            const float2 v01 = __half22float2(*(const __half2*)&vr[u].x);
+            const float2 v23 = __half22float2(*(const __half2*)&vr[u].y);
+            ls += e;
+            acc[0] = fmaf(e, v01.x, acc[0]);
+            acc[1] = fmaf(e, v01.y, acc[1]);
+            acc[2] = fmaf(e, v23.x, acc[2]);
+            acc[3] = fmaf(e, v23.y, acc[3]);
+          }
+          m = mb;
+        }
+        *(float4*)(wsm + warp * kAttRow + 4 * lane) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        if (lane == 0) {
+          wsm[warp * kAttRow + kHD] = m;
+          wsm[warp * kAttRow + kHD + 1] = ls;
+        }
+        __syncthreads();
+        if (tid < kHD) {  // combine the warps in warp order
+          float M = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < kSWarps; ++w) M = fmaxf(M, wsm[w * kAttRow + kHD]);
+          float o = 0.f, Ls = 0.f;
+#pragma unroll
+          for (int w = 0; w < kSWarps; ++w) {
+            const float mw = wsm[w * kAttRow + kHD];
+            const float wt = mw == -INFINITY ? 0.f : __expf(mw - M);
+            o = fmaf(wt, wsm[w * kAttRow + tid], o);
+            Ls = fmaf(wt, wsm[w * kAttRow + kHD + 1], Ls);
+          }
+          float* dst = pl.attp + ((size_t)hh * cph + j) * kAttRow;
+          dst[tid] = o;
+          if (tid == 0) {
+            dst[kHD] = M;
+            dst[kHD + 1] = Ls;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    grid_arrive();
+  };
+
+  // ---- the step ------------------------------------------------------------------------
+  const int d = pl.d;
+  const float inv_d = 1.f / (float)d;
+  // Residual prologue of an RMSNorm'd GEMV: a = hsrc (+ the partial slots of
+  // phase pph); the CTA's share of a is stored to hdst; returns the CTA-wide sum
+  // of squares' per-thread part and digitises a * nw.
+  struct ResRaw {
+    float4 h, w;
+    Slot4 p;
+  };
+  auto residual_prologue = [&](int ph, const float* hsrc, int pph, float* hdst, const float* nw) {
+    float ss = 0.f;
+    digitize_rows(
+        pl.S[ph], std::integral_constant<int, 2>{},
+        [&](int it) {
+          ResRaw r;
+          const uint32_t c = min(4u * it, (uint32_t)d - 4u);
+          r.h = ldcg4(hsrc + c);
+          r.w = __ldg((const float4*)(nw + c));
+          r.p = slot_load4(pph < 0 ? 3 : pph, c);
+          return r;
+        },
+        [&](int it, const ResRaw& r, float (&v)[4]) {
+          const uint32_t c = 4u * it;
+          if ((int)c < d) {
+            float4 a = r.h;
+            if (pph >= 0) add4(a, slot_val4(r.p));
+            if ((uint32_t)it - cta * pl.own_q < pl.own_q) *(float4*)(hdst + c) = a;
+            ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+            v[0] = a.x * r.w.x; v[1] = a.y * r.w.y; v[2] = a.z * r.w.z; v[3] = a.w * r.w.w;
+          } else {
+            v[0] = v[1] = v[2] = v[3] = 0.f;
+          }
+        });
+    return ss;
+  };
+  struct AttRaw {
+    float4 a[kMaxCph];
+    float2 ml[kMaxCph];
+  };
+  struct GuRaw {
+    Slot4 g, u;
+  };
+  float rinv1 = 0.f, rinv2 = 0.f;
+  for (int l = 0; l < pl.L; ++l) {
+    const float* const n1 = (const float*)ltab[l * kLtab + 8];
+    const float* const n2 = (const float*)ltab[l * kLtab + 9];
+#pragma unroll 1
+    for (int st = 0; st < 4; ++st) {  // one call site of the GEMV loop (code size)
+      if (st == 0) {
+        // QKV: h (layer input) = h' of the previous layer + its down_proj partials
+        const float ss = residual_prologue(0, l == 0 ? pl.h_in : pl.hx, l == 0 ? -1 : 3, pl.hy, n1);
+        rinv1 = rsqrtf(block_sum(ss) * inv_d + pl.eps);
+        prefetch_kv(l);
+      } else if (st == 1) {
+        // o_proj: combine the attention partials of each head
+        const int cph = pl.cph;
+        digitize_rows(
+            pl.S[1], std::integral_constant<int, 2>{},
+            [&](int it) {
+              AttRaw r;
+              const uint32_t c = min(4u * it, (uint32_t)d - 4u);
+              const float* src = pl.attp + (size_t)(c / kHD) * cph * kAttRow;
+#pragma unroll
+              for (int j = 0; j < kMaxCph; ++j) {
+                const int jj = min(j, cph - 1);
+                r.a[j] = ldcg4(src + jj * kAttRow + (c % kHD));
+                r.ml[j] = __ldcg((const float2*)(src + jj * kAttRow + kHD));
+              }
+              return r;
+            },
+            [&](int it, const AttRaw& r, float (&v)[4]) {
+              float M = -INFINITY;
+#pragma unroll
+              for (int j = 0; j < kMaxCph; ++j)
+                if (j < cph) M = fmaxf(M, r.ml[j].x);
+              float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+              float Ls = 0.f;
+#pragma unroll
+              for (int j = 0; j < kMaxCph; ++j) {
+                if (j < cph) {
+                  const float wt = r.ml[j].x == -INFINITY ? 0.f : __expf(r.ml[j].x - M);
+                  o.x = fmaf(wt, r.a[j].x, o.x); o.y = fmaf(wt, r.a[j].y, o.y);
+                  o.z = fmaf(wt, r.a[j].z, o.z); o.w = fmaf(wt, r.a[j].w, o.w);
+                  Ls = fmaf(wt, r.ml[j].y, Ls);
+                }
+              }
+              const float il = 4 * it < d ? 1.f / Ls : 0.f;
+              v[0] = o.x * il; v[1] = o.y * il; v[2] = o.z * il; v[3] = o.w * il;
+            });
+        __syncthreads();
+      } else if (st == 2) {
+        // gate|up: h' = h + o_proj partials
+        const float ss = residual_prologue(2, pl.hy, 1, pl.hx, n2);
+        rinv2 = rsqrtf(block_sum(ss) * inv_d + pl.eps);
+      } else {
+        // down_proj: SwiGLU of the gate|up partials (x rinv)
+        const int ffn = pl.ffn;
+        digitize_rows(
+            pl.S[3], std::integral_constant<int, 3>{},
+            [&](int it) {
+              GuRaw r;
+              const uint32_t c = min(4u * it, (uint32_t)ffn - 4u);
+              r.g = slot_load4(2, c);
+              r.u = slot_load4(2, (uint32_t)ffn + c);
+              return r;
+            },
+            [&](int it, const GuRaw& r, float (&v)[4]) {
+              if (4 * it < ffn) {
+                const float4 g = slot_val4(r.g), u = slot_val4(r.u);
+                const float gg[4] = {g.x * rinv2, g.y * rinv2, g.z * rinv2, g.w * rinv2};
+                const float uu[4] = {u.x * rinv2, u.y * rinv2, u.z * rinv2, u.w * rinv2};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = gg[i] / (1.f + __expf(-gg[i])) * uu[i];
+              } else {
+                v[0] = v[1] = v[2] = v[3] = 0.f;
+              }
+            });
+        __syncthreads();
+      }
+      stamp(2);
+      gemv_phase(st);
+      grid_wait();
+      if (st == 0) {
+        attention(l, rinv1);
+        grid_wait();
+      }
+    }
+  }
+  // the step's output: h' of the last layer + its down_proj partials
+  for (uint32_t it = cta * kSThreads + tid; it < (uint32_t)d / 4; it += G * kSThreads) {
+    float4 a = ldcg4(pl.hx + 4 * it);
+    add4(a, slot_val4(slot_load4(3, 4 * it)));
+    *(float4*)(pl.h_out + 4 * it) = a;
+  }
+  // re-arm the barrier for the next launch: the last CTA to leave resets it
+  __syncthreads();
+  if (tid == 0) {
+    if (atomicAdd(pl.bar + 2, 1u) == G - 1) {
+      pl.bar[0] = 0u;
+      pl.bar[2] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace
+}  // namespace qigen
+
+using namespace qigen;
+
+struct qigen_decode_stack {
+  SPlan plan{};
+  void* blob = nullptr;   // layer table | partial buffers | residuals | barrier words
+  size_t smem = 0;
+  int bits = 0, gps = 0;
+};
+
+// tuning aids (per calling thread): supersteps per weight stage (1 or 2), ring
+// depth cap
+static thread_local int g_stack_sss = 2;
+static thread_local int g_stack_depth = 8;
+extern "C" int qigen_debug_stack_tuning(int sss, int depth) {
+  g_stack_sss = sss == 1 ? 1 : 2;
+  g_stack_depth = depth < 2 ? 2 : depth;
+  return QIGEN_OK;
+}
+
+template <int B, int G>
+static int stack_launch(const qigen_decode_stack* s, const SPlan& pl, cudaStream_t st) {
+  static OncePerDevice once;
+  const int rc = once.run([]() -> int {
+    QIGEN_CUDA_RET(cudaFuncSetAttribute(decode_stack_kernel<B, G>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    return QIGEN_OK;
+  });
+  if (rc) return rc;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeCooperative;
+  at.val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)pl.G, 1, 1);
+  cfg.blockDim = dim3(kSThreads, 1, 1);
+  cfg.dynamicSmemBytes = s->smem;
+  cfg.stream = st;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  QIGEN_CUDA_RET(cudaLaunchKernelEx(&cfg, decode_stack_kernel<B, G>, pl));
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
+                                         const qigen_stack_layer* layers,
+                                         qigen_decode_stack** out) {
+  QIGEN_CHECK_ARG(desc && layers && out, QIGEN_ERR_ARG, "null pointer");
+  const qigen_stack_desc& e = *desc;
+  QIGEN_CHECK_ARG(e.bits == 2 || e.bits == 3 || e.bits == 4, QIGEN_ERR_CONFIG,
+                  "bits must be one of (2, 3, 4), got %d", e.bits);
+  QIGEN_CHECK_ARG(e.group_size == 32 || e.group_size == 64 || e.group_size == 128,
+                  QIGEN_ERR_UNSUPPORTED, "decode stack: group size must be 32, 64 or 128");
+  QIGEN_CHECK_ARG(e.layers > 0 && e.d_model > 0 && e.heads > 0 && e.ffn > 0 && e.ctx > 0,
+                  QIGEN_ERR_ARG, "decode stack: empty model");
+  QIGEN_CHECK_ARG(e.head_dim == kHD && (int64_t)e.heads * kHD == e.d_model, QIGEN_ERR_UNSUPPORTED,
+                  "decode stack: head_dim must be 128 and heads * 128 == d_model");
+  QIGEN_CHECK_ARG(e.d_model % 16 == 0 && e.ffn % 16 == 0 && e.d_model % e.group_size == 0 &&
+                      e.ffn % e.group_size == 0,
+                  QIGEN_ERR_UNSUPPORTED, "decode stack: d_model / ffn alignment");
+  int dev = 0, sms = 0;
+  QIGEN_CUDA_RET(cudaGetDevice(&dev));
+  QIGEN_CUDA_RET(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  auto* s = new qigen_decode_stack();
+  SPlan& pl = s->plan;
+  pl.L = e.layers;
+  pl.d = e.d_model;
+  pl.H = e.heads;
+  pl.ffn = e.ffn;
+  pl.ctx = (int)e.ctx;
+  // one CTA per SM, fewer for small models: with at least one whole panel of
+  // every phase per CTA a panel spans at most two CTAs (two partial slots)
+  sms = (int)std::min<int64_t>(sms, std::min<int64_t>(e.d_model, 2 * (int64_t)e.ffn) / 16);
+  pl.G = sms;
+  pl.eps = e.eps;
+  pl.cph = std::max(1, std::min(kMaxCph, sms / e.heads));
+  s->bits = e.bits;
+  s->gps = (int)(256 / e.group_size);
+  const int64_t Kd[4] = {e.d_model, e.d_model, e.d_model, e.ffn};
+  const int64_t Nd[4] = {3 * (int64_t)e.d_model, e.d_model, 2 * (int64_t)e.ffn, e.d_model};
+  const uint32_t GW = (uint32_t)sms * kSWarps;
+  uint32_t smax = 0;
+  int nslot[4];
+  std::vector<uint32_t> ctab((size_t)sms * kCtab, 0u), two;
+  for (int ph = 0; ph < 4; ++ph) {
+    pl.P[ph] = (uint32_t)panels(Nd[ph]);
+    pl.S[ph] = (uint32_t)supersteps(Kd[ph]);
+    pl.T[ph] = pl.P[ph] * pl.S[ph];
+    pl.pstride[ph] = pl.P[ph] * 16;
+    smax = std::max(smax, pl.S[ph]);
+    if ((uint64_t)(pl.T[ph] + 1) * GW >= (1ull << 32)) {
+      delete s;
+      QIGEN_CHECK_ARG(false, QIGEN_ERR_UNSUPPORTED, "decode stack: model too large");
+    }
+    // segments per warp and slots per column of the static partition
+    const uint32_t per = (pl.T[ph] + GW - 1) / GW;
+    const int segs = (int)((per + pl.S[ph] - 2) / pl.S[ph]) + 1;
+    int ns = 1;
+    pl.two_off[ph] = (uint32_t)two.size();
+    two.resize(two.size() + (pl.P[ph] + 31) / 32, 0u);
+    for (uint32_t p = 0; p < pl.P[ph]; ++p) {
+      const uint32_t c0 = warp_of(p * pl.S[ph], pl.T[ph], GW) / kSWarps;
+      const uint32_t c1 = warp_of(p * pl.S[ph] + pl.S[ph] - 1, pl.T[ph], GW) / kSWarps;
+      ns = std::max(ns, (int)(c1 - c0 + 1));
+      if (c1 != c0) two[pl.two_off[ph] + p / 32] |= 1u << (p % 32);
+    }
+    for (int c = 0; c < sms; ++c) {
+      uint32_t* row = &ctab[(size_t)c * kCtab + ph * kCrow];
+      for (int w = 0; w <= kSWarps; ++w) row[w] = lo_of((uint32_t)c * kSWarps + w, pl.T[ph], GW);
+      for (int w = 0; w < kSWarps; ++w) row[17 + w] = row[w] / pl.S[ph];
+      row[33] = row[16] > row[0] ? (row[16] - 1) / pl.S[ph] - row[17] + 1 : 0u;
+      if (row[33] * 16 > (uint32_t)kSThreads) ns = kMaxSlot + 1;  // (rejected below)
+    }
+    const uint32_t per_cta = (pl.T[ph] + sms - 1) / sms;
+    const uint32_t npan = (per_cta + pl.S[ph] - 2) / pl.S[ph] + 1;
+    if (segs > kMaxSeg || ns > kMaxSlot || npan * 16 > (uint32_t)kSThreads) {
+      delete s;
+      QIGEN_CHECK_ARG(false, QIGEN_ERR_UNSUPPORTED,
+                      "decode stack: shape outside the static partition's limits");
+    }
+    nslot[ph] = ns;
+  }
+  // shared memory: records | rings | warp partials | red | barriers | layer table
+  const size_t xrec = std::max<size_t>((size_t)smax * kSRec, kAttScratch);
+  const size_t xrec_al = (xrec + 127) / 128 * 128;
+  int sss = g_stack_sss, depth = 0;
+  size_t slot = 0;
+  pl.two_words = (uint32_t)two.size();
+  pl.own_q = (uint32_t)((e.d_model / 4 + sms - 1) / sms);
+  const size_t fixed = xrec_al + kSWarps * kMaxSeg * 16 * 4 + 32 * 4 +
+                       (size_t)e.layers * kLtab * sizeof(void*) + kCtab * 4 + two.size() * 4;
+  const size_t budget = 227 * 1024;
+  for (; sss >= 1 && depth < 2; --sss) {  // 2-superstep stages unless only 1-superstep ones fit
+    slot = (size_t)sss * (e.bits * 512 + s->gps * 128);
+    for (int dd = std::min(g_stack_depth, 16); dd >= 2; --dd)
+      if (fixed + (size_t)kSWarps * dd * (slot + 8) <= budget) {
+        depth = dd;
+        break;
+      }
+    if (depth >= 2) break;
+  }
+  if (depth < 2) {
+    delete s;
+    QIGEN_CHECK_ARG(false, QIGEN_ERR_UNSUPPORTED, "decode stack: shared memory does not fit");
+  }
+  pl.depth = depth;
+  pl.sss = sss;
+  pl.slot_bytes = (uint32_t)slot;
+  pl.xrec_bytes = (uint32_t)xrec_al;
+  s->smem = fixed + (size_t)kSWarps * depth * (slot + 8);
+  // device blob
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) / 256 * 256;
+    return o;
+  };
+  const size_t o_lay = take((size_t)e.layers * sizeof(SLayer));
+  size_t o_part[4];
+  for (int ph = 0; ph < 4; ++ph) o_part[ph] = take((size_t)nslot[ph] * pl.pstride[ph] * 4);
+  const size_t o_att = take((size_t)e.heads * pl.cph * kAttRow * 4);
+  const size_t o_hx = take((size_t)e.d_model * 4), o_hy = take((size_t)e.d_model * 4);
+  const size_t o_bar = take(256);
+  const size_t o_ctab = take(ctab.size() * 4), o_two = take(two.size() * 4);
+  cudaError_t ce = cudaMalloc(&s->blob, off);
+  if (ce != cudaSuccess) {
+    delete s;
+    QIGEN_CUDA_RET(ce);
+  }
+  std::vector<SLayer> tab(e.layers);
+  for (int l = 0; l < e.layers; ++l) {
+    for (int ph = 0; ph < 4; ++ph) {
+      if (!layers[l].qw[ph] || !layers[l].qsz[ph]) {
+        cudaFree(s->blob);
+        delete s;
+        QIGEN_CHECK_ARG(false, QIGEN_ERR_ARG, "decode stack: layer %d has a null weight", l);
+      }
+      tab[l].qw[ph] = (const char*)layers[l].qw[ph];
+      tab[l].qsz[ph] = (const char*)layers[l].qsz[ph];
+    }
+    tab[l].n1 = layers[l].norm1;
+    tab[l].n2 = layers[l].norm2;
+    tab[l].kc = (__half*)layers[l].k_cache;
+    tab[l].vc = (__half*)layers[l].v_cache;
+  }
+  char* b = (char*)s->blob;
+  cudaMemset(b, 0, off);
+  ce = cudaMemcpy(b + o_lay, tab.data(), tab.size() * sizeof(SLayer), cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(b + o_ctab, ctab.data(), ctab.size() * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(b + o_two, two.data(), two.size() * 4, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    cudaFree(s->blob);
+    delete s;
+    QIGEN_CUDA_RET(ce);
+  }
+  pl.layers = (const SLayer*)(b + o_lay);
+  for (int ph = 0; ph < 4; ++ph) pl.part[ph] = (float*)(b + o_part[ph]);
+  pl.attp = (float*)(b + o_att);
+  pl.hx = (float*)(b + o_hx);
+  pl.hy = (float*)(b + o_hy);
+  pl.bar = (unsigned int*)(b + o_bar);
+  pl.ctab = (const uint32_t*)(b + o_ctab);
+  pl.two = (const uint32_t*)(b + o_two);
+  *out = s;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_decode_stack_run(const qigen_decode_stack* s, const float* h_in, float* h_out,
+                                      const float* cosv, const float* sinv, int64_t pos,
+                                      float scale, void* stream) {
+  QIGEN_CHECK_ARG(s && h_in && h_out && cosv && sinv, QIGEN_ERR_ARG, "null pointer");
+  QIGEN_CHECK_ARG(pos >= 0 && pos < s->plan.ctx, QIGEN_ERR_ARG, "position outside the KV cache");
+  SPlan pl = s->plan;
+  pl.h_in = h_in;
+  pl.h_out = h_out;
+  pl.cosv = cosv;
+  pl.sinv = sinv;
+  pl.pos = (int)pos;
+  pl.scale = scale;
+  pl.trace = g_trace;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (s->bits * 16 + s->gps) {
+#define QS_CASE(B, G) \
+  case B * 16 + G: return stack_launch<B, G>(s, pl, st);
+    QS_CASE(2, 2) QS_CASE(2, 4) QS_CASE(2, 8)
+    QS_CASE(3, 2) QS_CASE(3, 4) QS_CASE(3, 8)
+    QS_CASE(4, 2) QS_CASE(4, 4) QS_CASE(4, 8)
+#undef QS_CASE
+    default: break;
+  }
+  set_error("decode stack: unsupported configuration");
+  return QIGEN_ERR_UNSUPPORTED;
+}
+
+extern "C" int qigen_decode_stack_error(const qigen_decode_stack* s, int* out) {
+  QIGEN_CHECK_ARG(s && out, QIGEN_ERR_ARG, "null pointer");
+  unsigned int w[4] = {};
+  QIGEN_CUDA_RET(cudaMemcpy(w, s->plan.bar, sizeof(w), cudaMemcpyDeviceToHost));
+  *out = (int)w[1];
+  if (w[1]) {  // a wait timed out: re-arm the counters
+    QIGEN_CUDA_RET(cudaMemset(s->plan.bar, 0, 16));
+  }
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_decode_stack_info(const qigen_decode_stack* s, int* grid, int* depth,
+                                       int* smem_bytes) {
+  QIGEN_CHECK_ARG(s, QIGEN_ERR_ARG, "null pointer");
+  if (grid) *grid = s->plan.G;
+  if (depth) *depth = s->plan.depth;
+  if (smem_bytes) *smem_bytes = (int)s->smem;
+  return QIGEN_OK;
+}
+
+extern "C" int qigen_decode_stack_destroy(qigen_decode_stack* s) {
+  if (!s) return QIGEN_OK;
+  if (s->blob) cudaFree(s->blob);
+  delete s;
+  return QIGEN_OK;
+}

@@ -403,7 +403,8 @@ class LlamaTP:
 
     def __init__(self, cfg: LlamaConfig, *, batch: int = 1, max_ctx: int = 1024, seed: int = 0,
                  device=None, tp: TP | None = None, backend=GpuBackend,
-                 kv_dtype=torch.float16, comm="auto", keep_logits: bool = True):
+                 kv_dtype=torch.float16, comm="auto", keep_logits: bool = True,
+                 stack: bool | None = None):
         self.cfg, self.B, self.max_ctx = cfg, batch, max_ctx
         self.tp = tp or TP()
         self.dev = torch.device(device) if device is not None else torch.device("cuda")
@@ -497,6 +498,14 @@ class LlamaTP:
                             if hd == 128 and (cfg.group is None or cfg.group >= 64) else None)
             self.ssc = ss_count(d)
             self.ss = [torch.zeros(batch * self.ssc, device=self.dev) for _ in range(2)]
+        # one GPU, one token: all layers as ONE persistent launch (csrc/decode_stack.cu);
+        # shapes outside its limits keep the per-op chain above
+        self.stack, self.stack_reason = None, "not requested"
+        if stack is None:
+            stack = os.environ.get("QIGEN_STACK", "1") == "1"
+        if (stack and self.tp.world == 1 and backend is GpuBackend and batch == 1
+                and kv_dtype == torch.float16):
+            self.stack = self._make_stack()
         self.fused_head = hasattr(backend, "lm_head") and self.dev.type == "cuda" and batch <= 8
         if self.fused_head:
             self.head_ws = backend.lm_head_workspace(self.v1 - self.v0, d, batch, self.dev)
@@ -518,6 +527,47 @@ class LlamaTP:
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, hd, 2, device=self.dev).float() / hd))
         ang = torch.arange(max_ctx, device=self.dev).float()[:, None] * inv[None, :]
         self.cos, self.sin = ang.cos(), ang.sin()  # [ctx, hd/2]
+
+    def _make_stack(self):
+        """The persistent decode-stack handle over this model's weights and KV
+        caches, or None where the kernel does not take the shape."""
+        import ctypes
+        from ._lib import StackDesc, StackLayer, UnsupportedError
+        cfg = self.cfg
+        if cfg.group is None:
+            return None
+        desc = StackDesc(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.head_dim, cfg.ffn, cfg.bits,
+                         cfg.group, self.max_ctx, cfg.norm_eps)
+        arr = (StackLayer * cfg.n_layers)()
+        for li, lay in enumerate(self.layers):
+            for j, k in enumerate(("qkv", "o", "gu", "down")):
+                arr[li].qw[j] = lay[k].pw.qw.data_ptr()
+                arr[li].qsz[j] = lay[k].pw.qsz.data_ptr()
+            arr[li].norm1, arr[li].norm2 = lay["n1"].data_ptr(), lay["n2"].data_ptr()
+            arr[li].k_cache = self.k_cache[li].data_ptr()
+            arr[li].v_cache = self.v_cache[li].data_ptr()
+        h = ctypes.c_void_p()
+        try:
+            call("qigen_decode_stack_create", ctypes.byref(desc), arr, ctypes.byref(h))
+        except UnsupportedError as e:
+            self.stack_reason = str(e)
+            return None
+        return h
+
+    def stack_error(self) -> int:
+        """Non-zero if a wait inside the persistent kernel timed out (synchronises)."""
+        import ctypes
+        v = ctypes.c_int()
+        call("qigen_decode_stack_error", self.stack, ctypes.byref(v))
+        return v.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "stack", None):
+                from ._lib import lib
+                lib().qigen_decode_stack_destroy(self.stack)
+        except Exception:  # noqa: BLE001
+            pass
 
     # -- accounting ---------------------------------------------------------
     def weight_bytes(self) -> int:
@@ -553,7 +603,12 @@ class LlamaTP:
         cos, sin = self.cos[pos], self.sin[pos]
         scale = 1.0 / math.sqrt(hd)
         att = torch.empty((B, self.nh * hd), dtype=torch.float32, device=self.dev)
-        for li, lay in enumerate(self.layers):
+        if self.stack is not None:  # every layer in one persistent launch
+            h_out = torch.empty_like(h)
+            call("qigen_decode_stack_run", self.stack, h.data_ptr(), h_out.data_ptr(),
+                 cos.data_ptr(), sin.data_ptr(), pos, float(scale), _dev.stream_handle())
+            h = h_out
+        for li, lay in enumerate(self.layers if self.stack is None else ()):
             if self.chained:
                 yield from self._layer_chained(li, lay, h, att, cos, sin, pos, scale)
                 continue

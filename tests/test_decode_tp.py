@@ -270,10 +270,10 @@ def test_chained_decode_matches_unchained():
                         bits=4, group=64)
     for B in (1, 2):
         os.environ["QIGEN_CHAIN"] = "0"
-        ref = D.LlamaTP(cfg, batch=B, max_ctx=40, seed=3, device="cuda")
+        ref = D.LlamaTP(cfg, batch=B, max_ctx=40, seed=3, device="cuda", stack=False)
         os.environ["QIGEN_CHAIN"] = "1"
-        m = D.LlamaTP(cfg, batch=B, max_ctx=40, seed=3, device="cuda")
-        assert m.chained and not ref.chained
+        m = D.LlamaTP(cfg, batch=B, max_ctx=40, seed=3, device="cuda", stack=False)
+        assert m.chained and not ref.chained and m.stack is None
         tok = torch.arange(B, device="cuda") * 131 + 7
         for pos in (30, 31):
             t1, t2 = ref.step(tok, pos), m.step(tok, pos)
@@ -281,3 +281,80 @@ def test_chained_decode_matches_unchained():
             assert ((l2 - l1).abs().max() / (1 + l1.abs().max())).item() < 1e-4
             assert torch.equal(t1, t2)
             tok = t1
+
+
+STACK_CASES = {
+    "d512_b4g128": (D.LlamaConfig(n_layers=2, d_model=512, n_heads=4, head_dim=128, ffn=1024,
+                                  vocab=512, bits=4, group=128), 64, 40),
+    "d1024_b4g64": (D.LlamaConfig(n_layers=3, d_model=1024, n_heads=8, head_dim=128, ffn=2816,
+                                  vocab=2000, bits=4, group=64), 40, 30),
+    "d1024_b3g64": (D.LlamaConfig(n_layers=2, d_model=1024, n_heads=8, head_dim=128, ffn=2816,
+                                  vocab=2000, bits=3, group=64), 300, 257),
+    "d1024_b2g32": (D.LlamaConfig(n_layers=2, d_model=1024, n_heads=8, head_dim=128, ffn=2816,
+                                  vocab=2000, bits=2, group=32), 40, 0),
+    "d1536_b3g128": (D.LlamaConfig(n_layers=2, d_model=1536, n_heads=12, head_dim=128, ffn=4224,
+                                   vocab=1000, bits=3, group=128), 100, 77),
+    "7b_2layers": (D.shrink(D.LLAMA_7B, n_layers=2), 514, 512),
+    "65b_1layer": (D.shrink(D.LLAMA_65B, n_layers=1), 1026, 1024),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", list(STACK_CASES))
+def test_decode_stack_matches_per_op_chain(case):
+    """The persistent decode stack (all layers in one launch, csrc/decode_stack.cu)
+    against the per-op kernel chain of the same model: same greedy tokens, logits
+    within 5e-4 of max|logit| (the stack applies 1/rms after the GEMV and reduces
+    in a different fixed order; the LM head rounds RMSNorm(h) to fp16, 2^-11
+    relative, before its GEMV: the bound of the TP test), the same appended KV rows, bit-identical
+    repeats, no wait timed out; two consecutive positions."""
+    cfg, ctx, pos = STACK_CASES[case]
+    ref = D.LlamaTP(cfg, batch=1, max_ctx=ctx, seed=13, device="cuda", stack=False)
+    m = D.LlamaTP(cfg, batch=1, max_ctx=ctx, seed=13, device="cuda", stack=True)
+    assert m.stack is not None and ref.stack is None, m.stack_reason
+    tok = torch.tensor([17], device="cuda")
+    for p in (pos, pos + 1):
+        t1, t2 = ref.step(tok, p), m.step(tok, p)
+        l1, l2 = ref.last_logits.double(), m.last_logits.double()
+        assert torch.isfinite(l2).all()
+        assert ((l2 - l1).abs().max() / (1 + l1.abs().max())).item() < 5e-4, (case, p)
+        assert torch.equal(t1, t2)
+        assert torch.allclose(m.k_cache[:, :, :, p].float(), ref.k_cache[:, :, :, p].float(),
+                              atol=2e-3, rtol=2e-3)
+        assert torch.allclose(m.v_cache[:, :, :, p].float(), ref.v_cache[:, :, :, p].float(),
+                              atol=2e-3, rtol=2e-3)
+        m.step(tok, p)  # deterministic: the same step again gives the same logits
+        assert torch.equal(m.last_logits.double(), l2)
+        tok = t1
+    assert m.stack_error() == 0
+
+
+@pytest.mark.gpu
+def test_decode_stack_in_a_cuda_graph():
+    """The persistent kernel (cooperative launch) is graph-capturable and
+    replays give the eager result."""
+    cfg, ctx, pos = STACK_CASES["d1024_b4g64"]
+    m = D.LlamaTP(cfg, batch=1, max_ctx=ctx, seed=13, device="cuda", stack=True)
+    tok = torch.tensor([5], device="cuda")
+    t0 = m.step(tok, pos).clone()
+    l0 = m.last_logits.clone()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        m.step(tok, pos)
+        with torch.cuda.graph(g, stream=s):
+            out = m.step(tok, pos)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, t0) and torch.equal(m.last_logits, l0)
+    assert m.stack_error() == 0
+
+
+def test_decode_stack_rejects_unsupported_shapes_cleanly():
+    """head_dim != 128 or ungrouped weights: no stack handle, the per-op chain runs
+    (checked here through the constructor's gating only; no GPU)."""
+    m = D.LlamaTP(TINY, batch=1, max_ctx=8, seed=1, device="cpu", backend=__import__(
+        "decode_backends").OracleBackend)
+    assert m.stack is None
