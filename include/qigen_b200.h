@@ -400,11 +400,14 @@ int qigen_decode_stack_run(const qigen_decode_stack* s, const float* h_in, float
 /* Synchronous: non-zero *out if a wait inside the last runs timed out (bit 0: grid
  * barrier, bit 1: weight stage); re-arms the handle. */
 int qigen_decode_stack_error(const qigen_decode_stack* s, int* out);
-int qigen_decode_stack_info(const qigen_decode_stack* s, int* grid, int* depth, int* smem_bytes);
+/* grid: CTAs; shape: ring stages * 100000 + supersteps per stage * 10000 + the K
+ * slabs of the four GEMV phases as digits (qkv, o, gate|up, down). */
+int qigen_decode_stack_info(const qigen_decode_stack* s, int* grid, int* shape, int* smem_bytes);
 int qigen_decode_stack_destroy(qigen_decode_stack* s);
 /* Tuning aid (per calling thread, read at create): supersteps per weight stage
- * (1 or 2) and the cap on ring stages per warp. */
-int qigen_debug_stack_tuning(int sss, int depth);
+ * (1 or 2), the cap on ring stages per warp and the K slabs (1, 2 or 4) wanted for
+ * the qkv, o, gate|up and down phases as four digits (default 2424). */
+int qigen_debug_stack_tuning(int sss, int depth, int ksl);
 
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */
 

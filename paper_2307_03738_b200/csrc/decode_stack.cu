@@ -10,21 +10,26 @@
 //     reference factorisation kernelgen.py:227-240 with exact IMMA partials)
 //     and the attention in between are PHASES separated by a grid barrier (one
 //     global counter, release/acquire);
-//   * a phase's work is its (panel, superstep) units in panel-major order,
-//     cut into equal contiguous ranges, one per warp of the grid (148 x 16):
-//     every warp streams its range through its own ring of TMA bulk-copy
-//     stages.  The schedule is static, so a warp's issue cursor simply runs
+//   * the CTAs form ksl groups (K slabs) x G / ksl panel ranges: group k owns
+//     the k-th slab of every phase's K supersteps, and within a group a phase's
+//     (panel, superstep-of-the-slab) units, in panel-major order, are cut into
+//     equal contiguous ranges, one per warp (e.g. 4 x 37 CTAs x 16 warps).  So a
+//     CTA only ever needs 1 / ksl of each activation vector (its prologue work
+//     and its shared-memory records shrink by ksl) and every warp streams its
+//     range through its own ring of TMA bulk-copy stages.  The schedule is static, so a warp's issue cursor simply runs
 //     ahead into the NEXT phases (and layers): weights keep streaming from HBM
 //     while the CTA sits in a barrier or digitises activations, and the rings
 //     never drain;
 //   * a warp's partial sums of a panel are reduced inside the CTA in warp
-//     order and stored as one partial per (CTA, panel) ("slot"); the consumer
-//     of the vector adds the slots in CTA order.  No atomics: deterministic;
+//     order and stored as one partial per (CTA, panel) ("slot": 2 per slab, a
+//     panel of a slab spans at most two CTAs); the consumer of the vector adds
+//     the slots in a fixed order.  No atomics: deterministic;
 //   * the consumer side of each phase ("prologue") is computed redundantly by
 //     every CTA straight into shared memory: residual add, RMSNorm weight,
 //     SwiGLU or the attention combine, then the fixed-point digit records of
-//     the whole K range (1152 B per 256 rows).  The 1/rms of an RMSNorm is
-//     applied to the GEMV's OUTPUT by its consumer (the GEMV is linear);
+//     the CTA's K slab (1152 B per 256 rows).  The 1/rms of an RMSNorm is
+//     applied to the GEMV's OUTPUT by its consumer (the GEMV is linear), from
+//     the per-slab sums of squares the groups publish;
 //   * attention: each head is split over cph CTAs by position; a warp keeps an
 //     online-softmax state over its positions, the CTA combines its warps and
 //     stores one partial per (head, chunk); the o_proj prologue combines them.
@@ -47,14 +52,16 @@ constexpr int kSWarps = 16;
 constexpr int kSThreads = kSWarps * 32;
 constexpr int kSRecDig = 1024;              // digit bytes per superstep record (1 token)
 constexpr int kSRec = kSRecDig + 8 * 16;    // + up to 8 units x {A, B, scale, 0}
-constexpr int kMaxSeg = 4;                  // panel segments per warp and phase
-constexpr int kMaxSlot = 2;                 // partials per output column (grid <= panels)
+constexpr int kMaxSeg = 8;                  // panel segments per warp and phase
+constexpr int kMaxKsl = 4;                  // K slabs (CTA groups)
+constexpr int kMaxSlot = 2;                 // partials per output column and slab
 constexpr int kAttRow = 132;                // floats per attention partial: acc[128], m, l, pad
 constexpr int kHD = 128;                    // head dimension
 constexpr int kMaxCph = 4;                  // position chunks (CTAs) per head
 constexpr int kAttScratch = (4 * kHD + kSWarps * kAttRow) * 4;
 constexpr int kLtab = 12;                   // pointers per layer in the shared-memory table
-constexpr int kCrow = 34;                   // per phase: lo[17], first panel[16], panel count
+constexpr int kCrow = 38;  // per phase: lo[17], first panel[16], panels, slab start, slab length,
+                           // slab index, CTA index within the slab group
 constexpr int kCtab = 4 * kCrow;
 
 struct SLayer {          // device table entry
@@ -69,6 +76,7 @@ struct SLayer {          // device table entry
 struct SPlan {
   const SLayer* layers;
   int L, d, H, ffn, ctx, cph, G;
+  int ksl[4];                  // K slabs (CTA groups) of each GEMV phase
   uint32_t P[4], S[4], T[4];   // panels, supersteps, units of the four GEMV phases
   uint32_t pstride[4];         // floats per partial slot (P * 16)
   float* part[4];              // [slots][P * 16]
@@ -77,8 +85,9 @@ struct SPlan {
   float* hy;                   // residual at layer entry (h)
   const uint32_t* ctab;        // [G][kCtab]: per CTA and phase, lo[17] | first panel[16] | panels
   const uint32_t* two;         // bit p of phase ph (word offset two_off[ph]): panel spans two CTAs
-  uint32_t two_off[4], two_words;
-  uint32_t own_q;              // residual items (4 floats) each CTA stores
+  uint32_t two_off[4], two_wp[4], two_words;  // per phase: word offset, words per slab
+  float* ssq;                  // [2][kMaxKsl]: per-slab sums of squares (norm1, norm2 input)
+  uint32_t own_q[4];           // residual items (4 floats) each CTA of a slab group stores
   unsigned int* bar;           // [0] barrier counter, [1] error word, [2] exit counter
   const float* h_in;
   float* h_out;
@@ -189,7 +198,6 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   float* red = wpart + kSWarps * kMaxSeg * 16;                         // [32]
   uint64_t* fullb = (uint64_t*)(red + 32);                             // [warp][depth]
   const char** ltab = (const char**)(fullb + kSWarps * depth);  // [L][12]: qw[4], qsz[4], n1, n2, kc, vc
-
   uint32_t* ctab = (uint32_t*)(ltab + pl.L * kLtab);            // this CTA's unit ranges
   uint32_t* twob = ctab + kCtab;                                // two-CTA panel bits
 
@@ -208,9 +216,10 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   uint64_t* full = fullb + warp * depth;
 
   // ---- issue cursor (lane 0): the warp's static stream of weight stages over
-  // all phases of all layers
+  // all phases of all layers.  Units are slab-local: unit u = (panel p, local
+  // superstep u - p Sk); the weights of panel p start S supersteps apart.
   int c_l = 0, c_ph = -1, islot = 0;
-  uint32_t c_u = 0, c_hi = 0, c_segend = 0;
+  uint32_t c_u = 0, c_hi = 0, c_segend = 0, c_sk = 0, c_jump = 0;
   bool c_done = false;
   const char *c_w = nullptr, *c_z = nullptr;
   auto next_phase = [&]() {
@@ -222,12 +231,17 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           return;
         }
       }
-      c_u = ctab[c_ph * kCrow + warp];
-      c_hi = ctab[c_ph * kCrow + warp + 1];
+      const uint32_t* row = ctab + c_ph * kCrow;
+      c_u = row[warp];
+      c_hi = row[warp + 1];
       if (c_hi > c_u) {
-        c_segend = (ctab[c_ph * kCrow + 17 + warp] + 1) * pl.S[c_ph];
-        c_w = ltab[c_l * kLtab + c_ph];
-        c_z = ltab[c_l * kLtab + 4 + c_ph];
+        const uint32_t p = row[17 + warp], s0 = row[34];
+        c_sk = row[35];
+        c_segend = (p + 1) * c_sk;
+        c_jump = pl.S[c_ph] - c_sk;  // supersteps of other slabs between two panels
+        const size_t first = (size_t)p * pl.S[c_ph] + s0 + (c_u - p * c_sk);
+        c_w = ltab[c_l * kLtab + c_ph] + first * WB;
+        c_z = ltab[c_l * kLtab + 4 + c_ph] + first * ZB;
         return;
       }
     }
@@ -238,12 +252,19 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     unsigned char* dst = ring + (size_t)islot * slot_bytes;
     uint64_t* bar = &full[islot];
     mbar_expect_tx(bar, nss * (WB + ZB));
-    bulk_g2s(dst, c_w + (size_t)c_u * WB, nss * WB, bar);
-    bulk_g2s(dst + sss * WB, c_z + (size_t)c_u * ZB, nss * ZB, bar);
+    bulk_g2s(dst, c_w, nss * WB, bar);
+    bulk_g2s(dst + sss * WB, c_z, nss * ZB, bar);
     if (++islot == depth) islot = 0;
     c_u += nss;
-    if (c_u == c_hi) next_phase();
-    else if (c_u == c_segend) c_segend += pl.S[c_ph];
+    c_w += nss * WB;
+    c_z += nss * ZB;
+    if (c_u == c_hi) {
+      next_phase();
+    } else if (c_u == c_segend) {
+      c_segend += c_sk;
+      c_w += (size_t)c_jump * WB;
+      c_z += (size_t)c_jump * ZB;
+    }
   };
   if (lane == 0) {
     next_phase();
@@ -283,48 +304,72 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     __syncthreads();
   };
 
-  // The four columns c .. c + 3 of a phase's output lie in one panel, which one
-  // CTA or two consecutive CTAs covered (the host keeps the grid <= the panel
-  // count): partial slot 0 and, if `two`, slot 1.  Loads are issued
-  // unconditionally (slot 0 twice for a single-CTA panel) so that a thread's
-  // loads of a whole prologue batch are in flight together.
-  auto two_slots = [&](int ph, uint32_t c) {
-    const uint32_t p = c >> 4;
-    return ((twob[pl.two_off[ph] + (p >> 5)] >> (p & 31)) & 1u) != 0u;
-  };
-  struct Slot4 {
-    float4 a, b;
-    bool two;
-  };
-  auto slot_load4 = [&](int ph, uint32_t c) {
-    Slot4 r;
-    r.two = two_slots(ph, c);
+  // A column block c .. c + 3 of a phase's output lies in one panel; each K slab
+  // contributed one partial (slot 2k) or two (2k + 1 too, when the panel spans
+  // two CTAs of group k; host-built bit table).  All loads of a sum are issued
+  // before the adds.
+  auto slot_sum4 = [&](int ph, uint32_t c) {
+    const uint32_t p = c >> 4, st = pl.pstride[ph];
+    const uint32_t* tb = twob + pl.two_off[ph] + (p >> 5);
     const float* src = pl.part[ph] + c;
-    r.a = ldcg4(src);
-    r.b = r.two ? ldcg4(src + pl.pstride[ph]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int ksl = pl.ksl[ph];
+    float4 a[kMaxKsl], b[kMaxKsl];
+#pragma unroll
+    for (int k = 0; k < kMaxKsl; ++k) {
+      const bool on = k < ksl;
+      const bool two = on && ((tb[k * pl.two_wp[ph]] >> (p & 31)) & 1u);
+      a[k] = on ? ldcg4(src + (size_t)(2 * k) * st) : make_float4(0.f, 0.f, 0.f, 0.f);
+      b[k] = two ? ldcg4(src + (size_t)(2 * k + 1) * st) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float4 r = a[0];
+    add4(r, b[0]);
+#pragma unroll
+    for (int k = 1; k < kMaxKsl; ++k) {
+      add4(r, a[k]);
+      add4(r, b[k]);
+    }
     return r;
   };
-  auto slot_val4 = [](const Slot4& r) {
-    float4 a = r.a;
-    if (r.two) add4(a, r.b);
-    return a;
-  };
   auto slot_sum1 = [&](int ph, uint32_t c) {  // one column
-    const bool two = two_slots(ph, c);
-    const float a = __ldcg(pl.part[ph] + c);
-    const float b = two ? __ldcg(pl.part[ph] + pl.pstride[ph] + c) : 0.f;
-    return two ? a + b : a;
+    const uint32_t p = c >> 4, st = pl.pstride[ph];
+    const uint32_t* tb = twob + pl.two_off[ph] + (p >> 5);
+    const float* src = pl.part[ph] + c;
+    const int ksl = pl.ksl[ph];
+    float a[kMaxKsl], b[kMaxKsl];
+#pragma unroll
+    for (int k = 0; k < kMaxKsl; ++k) {
+      const bool on = k < ksl;
+      const bool two = on && ((tb[k * pl.two_wp[ph]] >> (p & 31)) & 1u);
+      a[k] = on ? __ldcg(src + (size_t)(2 * k) * st) : 0.f;
+      b[k] = two ? __ldcg(src + (size_t)(2 * k + 1) * st) : 0.f;
+    }
+    float r = a[0] + b[0];
+#pragma unroll
+    for (int k = 1; k < kMaxKsl; ++k) r += a[k] + b[k];
+    return r;
+  };
+  // 1 / rms of a residual from the per-slab sums of squares its prologue (of
+  // phase 0: norm1, phase 2: norm2) published
+  auto rinv_of = [&](int which) {
+    float ssum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxKsl; ++k)
+      if (k < pl.ksl[2 * which]) ssum += __ldcg(pl.ssq + which * kMaxKsl + k);
+    return rsqrtf(ssum / (float)pl.d + pl.eps);
   };
 
-  // Digitise a K vector into the shared-memory records: item it = rows 4 it ..
-  // 4 it + 3.  load(it) fetches the item's inputs (addresses clamped into the
-  // vector), finish(it, raw, v) turns them into the four values (zeros beyond
-  // K); UB items per thread are loaded before any is finished.
-  auto digitize_rows = [&](uint32_t S, auto ub_c, auto&& load, auto&& finish) {
+  // Digitise this CTA's K slab of a phase's input into the shared-memory
+  // records: item it = rows 4 it .. 4 it + 3 (absolute), record of local
+  // superstep (it >> 6) - s0.  load(it) fetches the item's inputs (addresses
+  // clamped into the vector), finish(it, raw, v) turns them into the four
+  // values (zeros beyond K); UB items per thread are loaded before any is
+  // finished.
+  auto digitize_rows = [&](int ph, auto ub_c, auto&& load, auto&& finish) {
     constexpr int UB = decltype(ub_c)::value;
     const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
-    const int nit = (int)S * 64;
-    for (int it0 = warp * 32; it0 < nit; it0 += kSThreads * UB) {
+    const int s0 = (int)ctab[ph * kCrow + 34], sk = (int)ctab[ph * kCrow + 35];
+    const int itb = s0 * 64, nit = itb + sk * 64;
+    for (int it0 = itb + warp * 32; it0 < nit; it0 += kSThreads * UB) {
       decltype(load(0)) r[UB];
 #pragma unroll
       for (int u = 0; u < UB; ++u) r[u] = load(min(it0 + u * kSThreads + lane, nit - 1));
@@ -335,7 +380,7 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           float v[4];
           finish(it, r[u], v);
           const Digits dg = digitize<IPU>(v, umask);
-          unsigned char* rec = xrec + (size_t)(it >> 6) * kSRec;
+          unsigned char* rec = xrec + (size_t)((it >> 6) - s0) * kSRec;
           store_digits((uint32_t*)rec, (it >> 3) & 7, 0, 1, it & 7, dg);
           if ((it % IPU) == 0)
             ((float4*)(rec + kSRecDig))[(it & 63) / IPU] =
@@ -361,14 +406,14 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   int wslot = 0;
   uint32_t wph = 0;
   auto gemv_phase = [&](int ph) {
-    const uint32_t S = pl.S[ph];
     const uint32_t* row = ctab + ph * kCrow;
+    const uint32_t Sk = row[35];
     const uint32_t lo = row[warp], hi = row[warp + 1];
     uint32_t u = lo, p = row[17 + warp];
     int seg = 0;
     while (u < hi) {
-      uint32_t s = u - p * S;
-      const uint32_t seg_end = min(hi, (p + 1) * S);
+      uint32_t s = u - p * Sk;  // local superstep = record index
+      const uint32_t seg_end = min(hi, (p + 1) * Sk);
       float yv[2] = {0.f, 0.f};
       while (u < seg_end) {
         const uint32_t nss = min((uint32_t)sss, seg_end - u);
@@ -407,11 +452,12 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     }
     __syncthreads();
     stamp(3);
-    // the CTA's partial of every panel it touched: its warps' segments in warp order
+    // the CTA's partial of every panel it touched: its warps' segments in warp
+    // order; slot 2 slab (+ 1 when the panel started in the previous CTA)
     const uint32_t LO = row[0], HI = row[16], pf = row[17], npan = row[33];
-    if ((uint32_t)tid < npan * 16) {
-      const uint32_t pp = pf + tid / 16, col = tid % 16;
-      const uint32_t ua = max(LO, pp * S), ub = min(HI, (pp + 1) * S) - 1;
+    for (uint32_t idx = tid; idx < npan * 16; idx += kSThreads) {
+      const uint32_t pp = pf + idx / 16, col = idx % 16;
+      const uint32_t ua = max(LO, pp * Sk), ub = min(HI, (pp + 1) * Sk) - 1;
       float acc = 0.f;
 #pragma unroll
       for (int w = 0; w < kSWarps; ++w) {
@@ -419,8 +465,8 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
         if (hw > lw && hw > ua && lw <= ub)
           acc += wpart[((uint32_t)w * kMaxSeg + (pp - row[17 + w])) * 16 + col];
       }
-      // slot 1 when the panel started in the previous CTA
-      pl.part[ph][(pp * S < LO ? pl.pstride[ph] : 0u) + pp * 16 + col] = acc;
+      const uint32_t sl = 2 * row[36] + (pp * Sk < LO ? 1u : 0u);
+      pl.part[ph][(size_t)sl * pl.pstride[ph] + pp * 16 + col] = acc;
     }
     grid_arrive();
   };
@@ -441,8 +487,29 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     }
   };
 
-  // ---- attention of layer l (reads the QKV partials x rinv) -------------------------
-  auto attention = [&](int l, float rinv) {
+  // ---- attention of layer l (reads the QKV partials x 1 / rms) --------------------
+  // The first batch of cached K / V rows of this warp (first head of the CTA) is
+  // loaded into registers BEFORE the grid barrier of the QKV phase is awaited.
+  constexpr int NB = 8;
+  uint2 kr0[NB], vr0[NB];
+  auto attention_preload = [&](int l) {
+    const int cph = pl.cph, ngroups = (int)G / cph;
+    const int gi = (int)cta / cph, j = (int)cta % cph;
+    const int npos = pl.pos + 1, Lc = (npos + cph - 1) / cph;
+    const int p0 = j * Lc, p1 = min(min(p0 + Lc, npos), pl.pos);  // cached rows only
+    if (gi >= ngroups || gi >= pl.H) return;
+    const __half* kb = (const __half*)ltab[l * kLtab + 10] + (size_t)gi * pl.ctx * kHD + 4 * lane;
+    const __half* vb = (const __half*)ltab[l * kLtab + 11] + (size_t)gi * pl.ctx * kHD + 4 * lane;
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int pu = p0 + warp + kSWarps * u;
+      if (pu < p1) {
+        kr0[u] = __ldcg((const uint2*)(kb + (size_t)pu * kHD));
+        vr0[u] = __ldcg((const uint2*)(vb + (size_t)pu * kHD));
+      }
+    }
+  };
+  auto attention = [&](int l) {
     float* qs = (float*)xrec;       // rotated q (through f16)
     float* raw = qs + kHD;          // [3][128]: q, k, v of the new token
     float* wsm = raw + 3 * kHD;     // [warp][kAttRow]
@@ -454,6 +521,7 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     const int p0 = j * Lc, p1 = min(p0 + Lc, npos);
     const bool mine = pl.pos >= p0 && pl.pos < p1;  // this chunk holds the new token
     if (gi < ngroups) {
+      const float rinv = rinv_of(0);
       for (int hh = gi; hh < pl.H; hh += ngroups) {
         if (tid < 3 * kHD && (tid < kHD || mine))
           raw[tid] = slot_sum1(0, (uint32_t)(tid >> 7) * pl.d + (uint32_t)hh * kHD + (tid & 127)) * rinv;
@@ -482,15 +550,21 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
         float m = -INFINITY, ls = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
         const __half* kb = kc + (size_t)hh * pl.ctx * kHD + 4 * lane;
         const __half* vb = vc + (size_t)hh * pl.ctx * kHD + 4 * lane;
-        constexpr int NB = 8;
         for (int pp = p0 + warp; pp < p1; pp += kSWarps * NB) {
           uint2 kr[NB], vr[NB];
           float sc[NB];
+          const bool pre = hh == gi && pp == p0 + warp;  // the preloaded batch
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
             const int pu = min(pp + kSWarps * u, p1 - 1);
-            kr[u] = __ldcg((const uint2*)(kb + (size_t)pu * kHD));
-            vr[u] = __ldcg((const uint2*)(vb + (size_t)pu * kHD));
+            // (the new token's row, written above by this CTA, is never preloaded)
+            if (pre && pp + kSWarps * u < min(p1, pl.pos)) {
+              kr[u] = kr0[u];
+              vr[u] = vr0[u];
+            } else {
+              kr[u] = __ldcg((const uint2*)(kb + (size_t)pu * kHD));
+              vr[u] = __ldcg((const uint2*)(vb + (size_t)pu * kHD));
+            }
           }
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
@@ -558,48 +632,50 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
 
   // ---- the step ------------------------------------------------------------------------
   const int d = pl.d;
-  const float inv_d = 1.f / (float)d;
-  // Residual prologue of an RMSNorm'd GEMV: a = hsrc (+ the partial slots of
-  // phase pph); the CTA's share of a is stored to hdst; returns the CTA-wide sum
-  // of squares' per-thread part and digitises a * nw.
+  // Residual prologue of an RMSNorm'd GEMV over this CTA's slab of rows:
+  // a = hsrc (+ the partial slots of phase pph); the CTA's share of a is stored
+  // to hdst; a * nw is digitised; the slab's sum of squares goes to ssq[which]
+  // (applied as 1 / rms by the GEMV's consumer).
   struct ResRaw {
-    float4 h, w;
-    Slot4 p;
+    float4 h, w, p;
   };
-  auto residual_prologue = [&](int ph, const float* hsrc, int pph, float* hdst, const float* nw) {
+  auto residual_prologue = [&](int ph, const float* hsrc, int pph, float* hdst, const float* nw,
+                               int which) {
     float ss = 0.f;
+    const uint32_t own_q = pl.own_q[ph];
+    const uint32_t own0 = ctab[ph * kCrow + 34] * 64 + ctab[ph * kCrow + 37] * own_q;  // this CTA's items
     digitize_rows(
-        pl.S[ph], std::integral_constant<int, 2>{},
+        ph, std::integral_constant<int, 1>{},
         [&](int it) {
           ResRaw r;
           const uint32_t c = min(4u * it, (uint32_t)d - 4u);
           r.h = ldcg4(hsrc + c);
           r.w = __ldg((const float4*)(nw + c));
-          r.p = slot_load4(pph < 0 ? 3 : pph, c);
+          r.p = pph >= 0 ? slot_sum4(pph, c) : make_float4(0.f, 0.f, 0.f, 0.f);
           return r;
         },
         [&](int it, const ResRaw& r, float (&v)[4]) {
           const uint32_t c = 4u * it;
           if ((int)c < d) {
             float4 a = r.h;
-            if (pph >= 0) add4(a, slot_val4(r.p));
-            if ((uint32_t)it - cta * pl.own_q < pl.own_q) *(float4*)(hdst + c) = a;
+            add4(a, r.p);
+            if ((uint32_t)it - own0 < own_q) *(float4*)(hdst + c) = a;
             ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
             v[0] = a.x * r.w.x; v[1] = a.y * r.w.y; v[2] = a.z * r.w.z; v[3] = a.w * r.w.w;
           } else {
             v[0] = v[1] = v[2] = v[3] = 0.f;
           }
         });
-    return ss;
+    ss = block_sum(ss);
+    if (ctab[ph * kCrow + 37] == 0 && tid == 0) pl.ssq[which * kMaxKsl + ctab[ph * kCrow + 36]] = ss;
   };
   struct AttRaw {
     float4 a[kMaxCph];
     float2 ml[kMaxCph];
   };
   struct GuRaw {
-    Slot4 g, u;
+    float4 g, u;
   };
-  float rinv1 = 0.f, rinv2 = 0.f;
   for (int l = 0; l < pl.L; ++l) {
     const float* const n1 = (const float*)ltab[l * kLtab + 8];
     const float* const n2 = (const float*)ltab[l * kLtab + 9];
@@ -607,14 +683,13 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     for (int st = 0; st < 4; ++st) {  // one call site of the GEMV loop (code size)
       if (st == 0) {
         // QKV: h (layer input) = h' of the previous layer + its down_proj partials
-        const float ss = residual_prologue(0, l == 0 ? pl.h_in : pl.hx, l == 0 ? -1 : 3, pl.hy, n1);
-        rinv1 = rsqrtf(block_sum(ss) * inv_d + pl.eps);
+        residual_prologue(0, l == 0 ? pl.h_in : pl.hx, l == 0 ? -1 : 3, pl.hy, n1, 0);
         prefetch_kv(l);
       } else if (st == 1) {
         // o_proj: combine the attention partials of each head
         const int cph = pl.cph;
         digitize_rows(
-            pl.S[1], std::integral_constant<int, 2>{},
+            1, std::integral_constant<int, 1>{},
             [&](int it) {
               AttRaw r;
               const uint32_t c = min(4u * it, (uint32_t)d - 4u);
@@ -649,27 +724,26 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
         __syncthreads();
       } else if (st == 2) {
         // gate|up: h' = h + o_proj partials
-        const float ss = residual_prologue(2, pl.hy, 1, pl.hx, n2);
-        rinv2 = rsqrtf(block_sum(ss) * inv_d + pl.eps);
+        residual_prologue(2, pl.hy, 1, pl.hx, n2, 1);
       } else {
-        // down_proj: SwiGLU of the gate|up partials (x rinv)
+        // down_proj: SwiGLU of the gate|up partials (x 1 / rms)
         const int ffn = pl.ffn;
+        const float rinv2 = rinv_of(1);
         digitize_rows(
-            pl.S[3], std::integral_constant<int, 3>{},
+            3, std::integral_constant<int, 1>{},
             [&](int it) {
               GuRaw r;
               const uint32_t c = min(4u * it, (uint32_t)ffn - 4u);
-              r.g = slot_load4(2, c);
-              r.u = slot_load4(2, (uint32_t)ffn + c);
+              r.g = slot_sum4(2, c);
+              r.u = slot_sum4(2, (uint32_t)ffn + c);
               return r;
             },
             [&](int it, const GuRaw& r, float (&v)[4]) {
               if (4 * it < ffn) {
-                const float4 g = slot_val4(r.g), u = slot_val4(r.u);
-                const float gg[4] = {g.x * rinv2, g.y * rinv2, g.z * rinv2, g.w * rinv2};
-                const float uu[4] = {u.x * rinv2, u.y * rinv2, u.z * rinv2, u.w * rinv2};
+                const float gg[4] = {r.g.x * rinv2, r.g.y * rinv2, r.g.z * rinv2, r.g.w * rinv2};
+                const float uu[4] = {r.u.x * rinv2, r.u.y * rinv2, r.u.z * rinv2, r.u.w * rinv2};
 #pragma unroll
-                for (int i = 0; i < 4; ++i) v[i] = gg[i] / (1.f + __expf(-gg[i])) * uu[i];
+                for (int i = 0; i < 4; ++i) v[i] = __fdividef(gg[i], 1.f + __expf(-gg[i])) * uu[i];
               } else {
                 v[0] = v[1] = v[2] = v[3] = 0.f;
               }
@@ -678,18 +752,24 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
       }
       stamp(2);
       gemv_phase(st);
+      if (st == 0) attention_preload(l);
       grid_wait();
       if (st == 0) {
-        attention(l, rinv1);
+        attention(l);
         grid_wait();
       }
     }
   }
-  // the step's output: h' of the last layer + its down_proj partials
-  for (uint32_t it = cta * kSThreads + tid; it < (uint32_t)d / 4; it += G * kSThreads) {
-    float4 a = ldcg4(pl.hx + 4 * it);
-    add4(a, slot_val4(slot_load4(3, 4 * it)));
-    *(float4*)(pl.h_out + 4 * it) = a;
+  // the step's output: h' of the last layer + its down_proj partials (each CTA
+  // its share of its slab's rows)
+  {
+    const uint32_t own0 = ctab[34] * 64 + ctab[37] * pl.own_q[0];
+    const uint32_t own1 = min(own0 + pl.own_q[0], min((ctab[34] + ctab[35]) * 64, (uint32_t)d / 4));
+    for (uint32_t it = own0 + tid; it < own1; it += kSThreads) {
+      float4 a = ldcg4(pl.hx + 4 * it);
+      add4(a, slot_sum4(3, 4 * it));
+      *(float4*)(pl.h_out + 4 * it) = a;
+    }
   }
   // re-arm the barrier for the next launch: the last CTA to leave resets it
   __syncthreads();
@@ -718,9 +798,11 @@ struct qigen_decode_stack {
 // depth cap
 static thread_local int g_stack_sss = 2;
 static thread_local int g_stack_depth = 8;
-extern "C" int qigen_debug_stack_tuning(int sss, int depth) {
+static thread_local int g_stack_ksl = 2424;  // K slabs wanted for qkv, o, gate|up, down (digits)
+extern "C" int qigen_debug_stack_tuning(int sss, int depth, int ksl) {
   g_stack_sss = sss == 1 ? 1 : 2;
   g_stack_depth = depth < 2 ? 2 : depth;
+  g_stack_ksl = ksl < 1111 ? 1111 : ksl;
   return QIGEN_OK;
 }
 
@@ -763,80 +845,100 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   QIGEN_CHECK_ARG(e.d_model % 16 == 0 && e.ffn % 16 == 0 && e.d_model % e.group_size == 0 &&
                       e.ffn % e.group_size == 0,
                   QIGEN_ERR_UNSUPPORTED, "decode stack: d_model / ffn alignment");
+  for (int l = 0; l < e.layers; ++l)
+    for (int ph = 0; ph < 4; ++ph)
+      QIGEN_CHECK_ARG(layers[l].qw[ph] && layers[l].qsz[ph] && layers[l].norm1 &&
+                          layers[l].norm2 && layers[l].k_cache && layers[l].v_cache,
+                      QIGEN_ERR_ARG, "decode stack: layer %d has a null pointer", l);
   int dev = 0, sms = 0;
   QIGEN_CUDA_RET(cudaGetDevice(&dev));
   QIGEN_CUDA_RET(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  auto* s = new qigen_decode_stack();
-  SPlan& pl = s->plan;
+  const int64_t Kd[4] = {e.d_model, e.d_model, e.d_model, e.ffn};
+  const int64_t Nd[4] = {3 * (int64_t)e.d_model, e.d_model, 2 * (int64_t)e.ffn, e.d_model};
+  SPlan pl{};
+  for (int ph = 0; ph < 4; ++ph) {
+    pl.P[ph] = (uint32_t)panels(Nd[ph]);
+    pl.S[ph] = (uint32_t)supersteps(Kd[ph]);
+    pl.pstride[ph] = pl.P[ph] * 16;
+  }
+  // CTAs: at most the panels of the narrowest phase divided by its slab count,
+  // so that within a slab group a panel spans at most two CTAs (two slots per
+  // slab).  K slabs per phase: g_stack_ksl digits (qkv, o, gate|up, down), each
+  // reduced to a divisor of the grid that leaves every slab a superstep.
+  int G = sms;
+  for (int ph = 0; ph < 4; ++ph) G = (int)std::min<uint32_t>((uint32_t)G, pl.P[ph]);
+  G = std::max(1, G);
   pl.L = e.layers;
   pl.d = e.d_model;
   pl.H = e.heads;
   pl.ffn = e.ffn;
   pl.ctx = (int)e.ctx;
-  // one CTA per SM, fewer for small models: with at least one whole panel of
-  // every phase per CTA a panel spans at most two CTAs (two partial slots)
-  sms = (int)std::min<int64_t>(sms, std::min<int64_t>(e.d_model, 2 * (int64_t)e.ffn) / 16);
-  pl.G = sms;
+  pl.G = G;
   pl.eps = e.eps;
-  pl.cph = std::max(1, std::min(kMaxCph, sms / e.heads));
-  s->bits = e.bits;
-  s->gps = (int)(256 / e.group_size);
-  const int64_t Kd[4] = {e.d_model, e.d_model, e.d_model, e.ffn};
-  const int64_t Nd[4] = {3 * (int64_t)e.d_model, e.d_model, 2 * (int64_t)e.ffn, e.d_model};
-  const uint32_t GW = (uint32_t)sms * kSWarps;
-  uint32_t smax = 0;
-  int nslot[4];
-  std::vector<uint32_t> ctab((size_t)sms * kCtab, 0u), two;
+  pl.cph = std::max(1, std::min(kMaxCph, G / e.heads));
+  // per-CTA unit ranges and the two-CTA panel bits of the static partition
+  std::vector<uint32_t> ctab((size_t)G * kCtab, 0u), two;
+  uint32_t skmax = 0;
+  bool fits = true;
+  const int want[4] = {g_stack_ksl / 1000 % 10, g_stack_ksl / 100 % 10, g_stack_ksl / 10 % 10,
+                       g_stack_ksl % 10};
   for (int ph = 0; ph < 4; ++ph) {
-    pl.P[ph] = (uint32_t)panels(Nd[ph]);
-    pl.S[ph] = (uint32_t)supersteps(Kd[ph]);
-    pl.T[ph] = pl.P[ph] * pl.S[ph];
-    pl.pstride[ph] = pl.P[ph] * 16;
-    smax = std::max(smax, pl.S[ph]);
-    if ((uint64_t)(pl.T[ph] + 1) * GW >= (1ull << 32)) {
-      delete s;
-      QIGEN_CHECK_ARG(false, QIGEN_ERR_UNSUPPORTED, "decode stack: model too large");
-    }
-    // segments per warp and slots per column of the static partition
-    const uint32_t per = (pl.T[ph] + GW - 1) / GW;
-    const int segs = (int)((per + pl.S[ph] - 2) / pl.S[ph]) + 1;
-    int ns = 1;
+    const uint32_t P = pl.P[ph], S = pl.S[ph];
+    int ksl = 1;
+    for (int k : {4, 2})
+      if (k <= want[ph] && G % k == 0 && S >= (uint32_t)k && P >= (uint32_t)(G / k)) {
+        ksl = k;
+        break;
+      }
+    pl.ksl[ph] = ksl;
+    const int GJ = G / ksl;
+    const uint32_t GWJ = (uint32_t)GJ * kSWarps;  // warps per slab group
+    pl.own_q[ph] = (uint32_t)(((S + ksl - 1) / ksl * 64 + GJ - 1) / GJ);
     pl.two_off[ph] = (uint32_t)two.size();
-    two.resize(two.size() + (pl.P[ph] + 31) / 32, 0u);
-    for (uint32_t p = 0; p < pl.P[ph]; ++p) {
-      const uint32_t c0 = warp_of(p * pl.S[ph], pl.T[ph], GW) / kSWarps;
-      const uint32_t c1 = warp_of(p * pl.S[ph] + pl.S[ph] - 1, pl.T[ph], GW) / kSWarps;
-      ns = std::max(ns, (int)(c1 - c0 + 1));
-      if (c1 != c0) two[pl.two_off[ph] + p / 32] |= 1u << (p % 32);
+    pl.two_wp[ph] = (P + 31) / 32;
+    two.resize(two.size() + (size_t)ksl * pl.two_wp[ph], 0u);
+    for (int k = 0; k < ksl; ++k) {
+      const uint32_t s0 = (uint32_t)((uint64_t)k * S / ksl), s1 = (uint32_t)((uint64_t)(k + 1) * S / ksl);
+      const uint32_t Sk = s1 - s0, T = P * Sk;
+      skmax = std::max(skmax, Sk);
+      if ((uint64_t)(T + 1) * GWJ >= (1ull << 32)) fits = false;
+      for (uint32_t p = 0; fits && p < P; ++p) {
+        const uint32_t c0 = warp_of(p * Sk, T, GWJ) / kSWarps;
+        const uint32_t c1 = warp_of(p * Sk + Sk - 1, T, GWJ) / kSWarps;
+        if (c1 - c0 + 1 > kMaxSlot) fits = false;
+        if (c1 != c0) two[pl.two_off[ph] + (size_t)k * pl.two_wp[ph] + p / 32] |= 1u << (p % 32);
+      }
+      for (int j = 0; fits && j < GJ; ++j) {
+        uint32_t* row = &ctab[(size_t)(k * GJ + j) * kCtab + ph * kCrow];
+        for (int w = 0; w <= kSWarps; ++w) row[w] = lo_of((uint32_t)j * kSWarps + w, T, GWJ);
+        for (int w = 0; w < kSWarps; ++w) {
+          row[17 + w] = row[w] / Sk;
+          // panel segments of warp w
+          if (row[w + 1] > row[w] && (row[w + 1] - 1) / Sk - row[17 + w] + 1 > (uint32_t)kMaxSeg)
+            fits = false;
+        }
+        row[33] = row[16] > row[0] ? (row[16] - 1) / Sk - row[17] + 1 : 0u;
+        row[34] = s0;
+        row[35] = Sk;
+        row[36] = (uint32_t)k;
+        row[37] = (uint32_t)j;
+      }
     }
-    for (int c = 0; c < sms; ++c) {
-      uint32_t* row = &ctab[(size_t)c * kCtab + ph * kCrow];
-      for (int w = 0; w <= kSWarps; ++w) row[w] = lo_of((uint32_t)c * kSWarps + w, pl.T[ph], GW);
-      for (int w = 0; w < kSWarps; ++w) row[17 + w] = row[w] / pl.S[ph];
-      row[33] = row[16] > row[0] ? (row[16] - 1) / pl.S[ph] - row[17] + 1 : 0u;
-      if (row[33] * 16 > (uint32_t)kSThreads) ns = kMaxSlot + 1;  // (rejected below)
-    }
-    const uint32_t per_cta = (pl.T[ph] + sms - 1) / sms;
-    const uint32_t npan = (per_cta + pl.S[ph] - 2) / pl.S[ph] + 1;
-    if (segs > kMaxSeg || ns > kMaxSlot || npan * 16 > (uint32_t)kSThreads) {
-      delete s;
-      QIGEN_CHECK_ARG(false, QIGEN_ERR_UNSUPPORTED,
-                      "decode stack: shape outside the static partition's limits");
-    }
-    nslot[ph] = ns;
   }
-  // shared memory: records | rings | warp partials | red | barriers | layer table
-  const size_t xrec = std::max<size_t>((size_t)smax * kSRec, kAttScratch);
+  QIGEN_CHECK_ARG(fits, QIGEN_ERR_UNSUPPORTED,
+                  "decode stack: shape outside the static partition's limits");
+  pl.two_words = (uint32_t)two.size();
+  // shared memory: records | rings | warp partials | red | barriers | tables
+  const size_t xrec = std::max<size_t>((size_t)skmax * kSRec, kAttScratch);
   const size_t xrec_al = (xrec + 127) / 128 * 128;
+  const int gps = (int)(256 / e.group_size);
   int sss = g_stack_sss, depth = 0;
   size_t slot = 0;
-  pl.two_words = (uint32_t)two.size();
-  pl.own_q = (uint32_t)((e.d_model / 4 + sms - 1) / sms);
   const size_t fixed = xrec_al + kSWarps * kMaxSeg * 16 * 4 + 32 * 4 +
                        (size_t)e.layers * kLtab * sizeof(void*) + kCtab * 4 + two.size() * 4;
   const size_t budget = 227 * 1024;
-  for (; sss >= 1 && depth < 2; --sss) {  // 2-superstep stages unless only 1-superstep ones fit
-    slot = (size_t)sss * (e.bits * 512 + s->gps * 128);
+  for (; sss >= 1; --sss) {  // 2-superstep stages unless only 1-superstep ones fit
+    slot = (size_t)sss * (e.bits * 512 + gps * 128);
     for (int dd = std::min(g_stack_depth, 16); dd >= 2; --dd)
       if (fixed + (size_t)kSWarps * dd * (slot + 8) <= budget) {
         depth = dd;
@@ -844,15 +946,11 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
       }
     if (depth >= 2) break;
   }
-  if (depth < 2) {
-    delete s;
-    QIGEN_CHECK_ARG(false, QIGEN_ERR_UNSUPPORTED, "decode stack: shared memory does not fit");
-  }
+  QIGEN_CHECK_ARG(depth >= 2, QIGEN_ERR_UNSUPPORTED, "decode stack: shared memory does not fit");
   pl.depth = depth;
   pl.sss = sss;
   pl.slot_bytes = (uint32_t)slot;
   pl.xrec_bytes = (uint32_t)xrec_al;
-  s->smem = fixed + (size_t)kSWarps * depth * (slot + 8);
   // device blob
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -862,24 +960,14 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   };
   const size_t o_lay = take((size_t)e.layers * sizeof(SLayer));
   size_t o_part[4];
-  for (int ph = 0; ph < 4; ++ph) o_part[ph] = take((size_t)nslot[ph] * pl.pstride[ph] * 4);
+  for (int ph = 0; ph < 4; ++ph) o_part[ph] = take((size_t)2 * pl.ksl[ph] * pl.pstride[ph] * 4);
   const size_t o_att = take((size_t)e.heads * pl.cph * kAttRow * 4);
   const size_t o_hx = take((size_t)e.d_model * 4), o_hy = take((size_t)e.d_model * 4);
-  const size_t o_bar = take(256);
+  const size_t o_bar = take(256), o_ssq = take(2 * kMaxKsl * 4);
   const size_t o_ctab = take(ctab.size() * 4), o_two = take(two.size() * 4);
-  cudaError_t ce = cudaMalloc(&s->blob, off);
-  if (ce != cudaSuccess) {
-    delete s;
-    QIGEN_CUDA_RET(ce);
-  }
   std::vector<SLayer> tab(e.layers);
   for (int l = 0; l < e.layers; ++l) {
     for (int ph = 0; ph < 4; ++ph) {
-      if (!layers[l].qw[ph] || !layers[l].qsz[ph]) {
-        cudaFree(s->blob);
-        delete s;
-        QIGEN_CHECK_ARG(false, QIGEN_ERR_ARG, "decode stack: layer %d has a null weight", l);
-      }
       tab[l].qw[ph] = (const char*)layers[l].qw[ph];
       tab[l].qsz[ph] = (const char*)layers[l].qsz[ph];
     }
@@ -888,15 +976,18 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
     tab[l].kc = (__half*)layers[l].k_cache;
     tab[l].vc = (__half*)layers[l].v_cache;
   }
+  auto* s = new qigen_decode_stack();
+  cudaError_t ce = cudaMalloc(&s->blob, off);
   char* b = (char*)s->blob;
-  cudaMemset(b, 0, off);
-  ce = cudaMemcpy(b + o_lay, tab.data(), tab.size() * sizeof(SLayer), cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) ce = cudaMemset(b, 0, off);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(b + o_lay, tab.data(), tab.size() * sizeof(SLayer), cudaMemcpyHostToDevice);
   if (ce == cudaSuccess)
     ce = cudaMemcpy(b + o_ctab, ctab.data(), ctab.size() * 4, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess)
     ce = cudaMemcpy(b + o_two, two.data(), two.size() * 4, cudaMemcpyHostToDevice);
   if (ce != cudaSuccess) {
-    cudaFree(s->blob);
+    if (s->blob) cudaFree(s->blob);
     delete s;
     QIGEN_CUDA_RET(ce);
   }
@@ -906,8 +997,13 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   pl.hx = (float*)(b + o_hx);
   pl.hy = (float*)(b + o_hy);
   pl.bar = (unsigned int*)(b + o_bar);
+  pl.ssq = (float*)(b + o_ssq);
   pl.ctab = (const uint32_t*)(b + o_ctab);
   pl.two = (const uint32_t*)(b + o_two);
+  s->plan = pl;
+  s->bits = e.bits;
+  s->gps = gps;
+  s->smem = fixed + (size_t)kSWarps * depth * (slot + 8);
   *out = s;
   return QIGEN_OK;
 }
@@ -954,7 +1050,9 @@ extern "C" int qigen_decode_stack_info(const qigen_decode_stack* s, int* grid, i
                                        int* smem_bytes) {
   QIGEN_CHECK_ARG(s, QIGEN_ERR_ARG, "null pointer");
   if (grid) *grid = s->plan.G;
-  if (depth) *depth = s->plan.depth;
+  if (depth)
+    *depth = s->plan.depth * 100000 + s->plan.sss * 10000 + s->plan.ksl[0] * 1000 +
+             s->plan.ksl[1] * 100 + s->plan.ksl[2] * 10 + s->plan.ksl[3];
   if (smem_bytes) *smem_bytes = (int)s->smem;
   return QIGEN_OK;
 }

@@ -2,7 +2,7 @@
 barrier, when the CTAs arrive and pass (globaltimer, us), i.e. per phase the
 prologue + compute time, the arrival spread and the barrier latency.
 
-  python tools/trace_stack.py [7b|65b] [layers] [sss] [depth]
+  python tools/trace_stack.py [7b|65b] [layers] [sss depth ksl]
 """
 import sys
 from pathlib import Path
@@ -17,8 +17,8 @@ from paper_2307_03738_b200 import _lib  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "7b"
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 Lb = _lib.lib()
-if len(sys.argv) > 4:
-    Lb.qigen_debug_stack_tuning(int(sys.argv[3]), int(sys.argv[4]))
+if len(sys.argv) > 5:
+    Lb.qigen_debug_stack_tuning(int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]))
 base, ctx = (D.LLAMA_7B, 512) if name == "7b" else (D.LLAMA_65B, 1024)
 cfg = D.shrink(base, n_layers=L)
 m = D.LlamaTP(cfg, batch=1, max_ctx=ctx + 1, seed=0, stack=True, keep_logits=False)
@@ -27,7 +27,7 @@ import ctypes
 gi, dp, sm = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
 Lb.qigen_decode_stack_info(m.stack, ctypes.byref(gi), ctypes.byref(dp), ctypes.byref(sm))
 G = gi.value
-print(f"{name} {L} layers: grid {G}, ring depth {dp.value}, smem {sm.value} B")
+print(f"{name} {L} layers: grid {G}, ring depth*100 + stage supersteps*10 + K slabs {dp.value}, smem {sm.value} B")
 tok = torch.tensor([3], device="cuda")
 nbar = 5 * L
 buf = torch.zeros(nbar * G * 4, dtype=torch.int64, device="cuda")
