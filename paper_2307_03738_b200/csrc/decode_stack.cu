@@ -476,8 +476,8 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   auto prefetch_kv = [&](int l) {
     const int cph = pl.cph, ngroups = (int)G / cph;
     const int gi = (int)cta / cph, j = (int)cta % cph;
-    const int npos = pl.pos + 1, Lc = (npos + cph - 1) / cph;
-    const int p0 = j * Lc, p1 = min(min(p0 + Lc, npos), pl.pos);  // cached rows only
+    const int Lc = (pl.pos + cph - 1) / cph;
+    const int p0 = j * Lc, p1 = min(p0 + Lc, pl.pos);  // cached rows of this chunk
     if (gi >= ngroups || p1 <= p0 || tid >= 2) return;
     const char* base = ltab[l * kLtab + 10 + tid];
     for (int hh = gi; hh < pl.H; hh += ngroups) {
@@ -488,16 +488,25 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   };
 
   // ---- attention of layer l (reads the QKV partials x 1 / rms) --------------------
-  // The first batch of cached K / V rows of this warp (first head of the CTA) is
-  // loaded into registers BEFORE the grid barrier of the QKV phase is awaited.
+  // A head's CACHED positions 0 .. pos - 1 are split over its cph CTAs, a CTA's
+  // chunk over its warps (position p0 + warp + 16 i); the new token is one more
+  // position, taken from shared memory by warp 0 of the last chunk's CTA (which
+  // also appends it to the cache).  The first batch of cached K / V rows of each
+  // warp (first head of the CTA) and the RoPE factors are loaded into registers
+  // BEFORE the grid barrier of the QKV phase is awaited.
   constexpr int NB = 8;
   uint2 kr0[NB], vr0[NB];
+  float rope_c = 0.f, rope_s = 0.f;
   auto attention_preload = [&](int l) {
     const int cph = pl.cph, ngroups = (int)G / cph;
     const int gi = (int)cta / cph, j = (int)cta % cph;
-    const int npos = pl.pos + 1, Lc = (npos + cph - 1) / cph;
-    const int p0 = j * Lc, p1 = min(min(p0 + Lc, npos), pl.pos);  // cached rows only
+    const int Lc = (pl.pos + cph - 1) / cph;
+    const int p0 = j * Lc, p1 = min(p0 + Lc, pl.pos);
     if (gi >= ngroups || gi >= pl.H) return;
+    if (tid < kHD / 2) {
+      rope_c = pl.cosv[tid];
+      rope_s = pl.sinv[tid];
+    }
     const __half* kb = (const __half*)ltab[l * kLtab + 10] + (size_t)gi * pl.ctx * kHD + 4 * lane;
     const __half* vb = (const __half*)ltab[l * kLtab + 11] + (size_t)gi * pl.ctx * kHD + 4 * lane;
 #pragma unroll
@@ -511,24 +520,25 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   };
   auto attention = [&](int l) {
     float* qs = (float*)xrec;       // rotated q (through f16)
-    float* raw = qs + kHD;          // [3][128]: q, k, v of the new token
+    float* raw = qs + kHD;          // [3][128]: q, k, v of the new token (k, v: as cached)
     float* wsm = raw + 3 * kHD;     // [warp][kAttRow]
     __half* const kc = (__half*)ltab[l * kLtab + 10];
     __half* const vc = (__half*)ltab[l * kLtab + 11];
     const int cph = pl.cph, ngroups = (int)G / cph;
     const int gi = (int)cta / cph, j = (int)cta % cph;
-    const int npos = pl.pos + 1, Lc = (npos + cph - 1) / cph;
-    const int p0 = j * Lc, p1 = min(p0 + Lc, npos);
-    const bool mine = pl.pos >= p0 && pl.pos < p1;  // this chunk holds the new token
+    const int Lc = (pl.pos + cph - 1) / cph;
+    const int p0 = j * Lc, p1 = min(p0 + Lc, pl.pos);  // cached rows of this chunk
+    const bool mine = j == cph - 1;                    // this CTA takes the new token
     if (gi < ngroups) {
       const float rinv = rinv_of(0);
       for (int hh = gi; hh < pl.H; hh += ngroups) {
         if (tid < 3 * kHD && (tid < kHD || mine))
           raw[tid] = slot_sum1(0, (uint32_t)(tid >> 7) * pl.d + (uint32_t)hh * kHD + (tid & 127)) * rinv;
         __syncthreads();
+        float k0 = 0.f, k1 = 0.f, v0 = 0.f, v1 = 0.f;
         if (tid < kHD / 2) {
           const int i = tid;
-          const float c = pl.cosv[i], s = pl.sinv[i];
+          const float c = rope_c, s = rope_s;
           // rotate-half with separately rounded products, q / k rounded through
           // f16 (decode_ops.cu attn_decode_kernel)
           auto rot_lo = [&](float x0, float x1) { return __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s)); };
@@ -537,15 +547,27 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           qs[i] = __half2float(__float2half_rn(rot_lo(q0, q1)));
           qs[i + kHD / 2] = __half2float(__float2half_rn(rot_hi(q0, q1)));
           if (mine) {  // append k, v
-            const float k0 = raw[kHD + i], k1 = raw[kHD + i + kHD / 2];
+            const float x0 = raw[kHD + i], x1 = raw[kHD + i + kHD / 2];
+            const __half hk0 = __float2half_rn(rot_lo(x0, x1)), hk1 = __float2half_rn(rot_hi(x0, x1));
+            const __half hv0 = __float2half_rn(raw[2 * kHD + i]);
+            const __half hv1 = __float2half_rn(raw[2 * kHD + i + kHD / 2]);
             const size_t g = ((size_t)hh * pl.ctx + pl.pos) * kHD;
-            kc[g + i] = __float2half_rn(rot_lo(k0, k1));
-            kc[g + i + kHD / 2] = __float2half_rn(rot_hi(k0, k1));
-            vc[g + i] = __float2half_rn(raw[2 * kHD + i]);
-            vc[g + i + kHD / 2] = __float2half_rn(raw[2 * kHD + i + kHD / 2]);
+            kc[g + i] = hk0;
+            kc[g + i + kHD / 2] = hk1;
+            vc[g + i] = hv0;
+            vc[g + i + kHD / 2] = hv1;
+            k0 = __half2float(hk0); k1 = __half2float(hk1);
+            v0 = __half2float(hv0); v1 = __half2float(hv1);
           }
         }
-        __syncthreads();
+        __syncthreads();  // every thread has read raw: k, v of the new token replace it
+        if (mine && tid < kHD / 2) {
+          raw[kHD + tid] = k0;
+          raw[kHD + tid + kHD / 2] = k1;
+          raw[2 * kHD + tid] = v0;
+          raw[2 * kHD + tid + kHD / 2] = v1;
+        }
+        stamp(2);
         const float4 q = *(const float4*)(qs + 4 * lane);
         float m = -INFINITY, ls = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
         const __half* kb = kc + (size_t)hh * pl.ctx * kHD + 4 * lane;
@@ -556,12 +578,11 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           const bool pre = hh == gi && pp == p0 + warp;  // the preloaded batch
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
-            const int pu = min(pp + kSWarps * u, p1 - 1);
-            // (the new token's row, written above by this CTA, is never preloaded)
-            if (pre && pp + kSWarps * u < min(p1, pl.pos)) {
+            if (pre) {
               kr[u] = kr0[u];
               vr[u] = vr0[u];
             } else {
+              const int pu = min(pp + kSWarps * u, p1 - 1);
               kr[u] = __ldcg((const uint2*)(kb + (size_t)pu * kHD));
               vr[u] = __ldcg((const uint2*)(vb + (size_t)pu * kHD));
             }
@@ -588,17 +609,37 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           for (int e = 0; e < 4; ++e) acc[e] *= corr;
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
-            const float e = __expf(sc[u] - mb);  // 0 for the masked tail
+            // masked tail: weight 0 (its registers may hold anything)
+            const float e = pp + kSWarps * u < p1 ? __expf(sc[u] - mb) : 0.f;
             const float2 v01 = __half22float2(*(const __half2*)&vr[u].x);
             const float2 v23 = __half22float2(*(const __half2*)&vr[u].y);
             ls += e;
-            acc[0] = fmaf(e, v01.x, acc[0]);
-            acc[1] = fmaf(e, v01.y, acc[1]);
-            acc[2] = fmaf(e, v23.x, acc[2]);
-            acc[3] = fmaf(e, v23.y, acc[3]);
+            acc[0] = e != 0.f ? fmaf(e, v01.x, acc[0]) : acc[0];
+            acc[1] = e != 0.f ? fmaf(e, v01.y, acc[1]) : acc[1];
+            acc[2] = e != 0.f ? fmaf(e, v23.x, acc[2]) : acc[2];
+            acc[3] = e != 0.f ? fmaf(e, v23.y, acc[3]) : acc[3];
           }
           m = mb;
         }
+        __syncthreads();  // the new token's k, v are in raw
+        if (mine && warp == 0) {  // the new token: one more position
+          const float4 kn = *(const float4*)(raw + kHD + 4 * lane);
+          const float4 vn = *(const float4*)(raw + 2 * kHD + 4 * lane);
+          float sc = q.x * kn.x + q.y * kn.y + q.z * kn.z + q.w * kn.w;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+          sc *= pl.scale;
+          const float mb = fmaxf(m, sc);
+          const float corr = m == -INFINITY ? 0.f : __expf(m - mb);
+          const float e = __expf(sc - mb);
+          ls = ls * corr + e;
+          acc[0] = fmaf(e, vn.x, acc[0] * corr);
+          acc[1] = fmaf(e, vn.y, acc[1] * corr);
+          acc[2] = fmaf(e, vn.z, acc[2] * corr);
+          acc[3] = fmaf(e, vn.w, acc[3] * corr);
+          m = mb;
+        }
+        stamp(3);
         *(float4*)(wsm + warp * kAttRow + 4 * lane) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         if (lane == 0) {
           wsm[warp * kAttRow + kHD] = m;

@@ -66,8 +66,8 @@ for b in range(nbar):
     work = arr.max() - (prev_pass if prev_pass is not None else 0.0)
     lat = pas.max() - arr.max()
     base = prev_pass if prev_pass is not None else 0.0
-    pro = (t[b, :, 2] - t0).max() - base if ph != "attn" else 0.0   # prologue done (last CTA)
-    loop = (t[b, :, 3] - t0).max() - base if ph != "attn" else 0.0  # GEMV loop done (last CTA)
+    pro = (t[b, :, 2] - t0).max() - base   # prologue done (last CTA); attention: q ready
+    loop = (t[b, :, 3] - t0).max() - base  # GEMV loop done (last CTA); attention: KV loop done (warp 0)
     tot.setdefault(ph, []).append((work, lat, arr.max() - arr.min(), pro, loop))
     if b < 10 or b >= nbar - 5:
         print(f"L{b // 5} {ph:5s} arrive {arr.min():8.2f}-{arr.max():8.2f} (spread {arr.max() - arr.min():5.2f})"
