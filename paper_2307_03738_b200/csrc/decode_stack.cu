@@ -55,10 +55,12 @@ constexpr int kSRec = kSRecDig + 8 * 16;    // + up to 8 units x {A, B, scale, 0
 constexpr int kMaxSeg = 8;                  // panel segments per warp and phase
 constexpr int kMaxKsl = 4;                  // K slabs (CTA groups)
 constexpr int kMaxSlot = 2;                 // partials per output column and slab
-constexpr int kAttRow = 132;                // floats per attention partial: acc[128], m, l, pad
+constexpr int kAttRow = 264;                // floats per attention partial: {value, flag} pairs of
+                                            // acc[128], m, l (+ pad); also the warps' smem rows
 constexpr int kHD = 128;                    // head dimension
 constexpr int kMaxCph = 4;                  // position chunks (CTAs) per head
-constexpr int kAttScratch = (4 * kHD + kSWarps * kAttRow) * 4;
+constexpr int kAttSm = 132;                 // floats per warp partial in shared memory: acc[128], m, l
+constexpr int kAttScratch = (4 * kHD + kSWarps * kAttSm) * 4;
 constexpr int kLtab = 12;                   // pointers per layer in the shared-memory table
 constexpr int kCrow = 38;  // per phase: lo[17], first panel[16], panels, slab start, slab length,
                            // slab index, CTA index within the slab group
@@ -79,16 +81,15 @@ struct SPlan {
   int ksl[4];                  // K slabs (CTA groups) of each GEMV phase
   uint32_t P[4], S[4], T[4];   // panels, supersteps, units of the four GEMV phases
   uint32_t pstride[4];         // floats per partial slot (P * 16)
-  float* part[4];              // [slots][P * 16]
-  float* attp;                 // [H][cph][kAttRow]
-  float* hx;                   // residual after o_proj (h')
-  float* hy;                   // residual at layer entry (h)
+  float* part[4];              // [3 buffer sets][2 ksl slots][P * 16] {value, flag}
+  float* attp;                 // [3][H][cph][kAttRow]
   const uint32_t* ctab;        // [G][kCtab]: per CTA and phase, lo[17] | first panel[16] | panels
   const uint32_t* two;         // bit p of phase ph (word offset two_off[ph]): panel spans two CTAs
   uint32_t two_off[4], two_wp[4], two_words;  // per phase: word offset, words per slab
-  float* ssq;                  // [2][kMaxKsl]: per-slab sums of squares (norm1, norm2 input)
+  float* ssq;                  // [3][2][kMaxKsl] {value, flag}: per-slab sums of squares (norm1, norm2 input)
   uint32_t own_q[4];           // residual items (4 floats) each CTA of a slab group stores
-  unsigned int* bar;           // [0] barrier counter, [1] error word, [2] exit counter
+  unsigned int* bar;           // [0] layers finished (all CTAs), [1] error word, [2] exit counter,
+                               // [3] launch epoch
   const float* h_in;
   float* h_out;
   const float* cosv;
@@ -96,7 +97,7 @@ struct SPlan {
   int pos;
   float scale, eps;
   int depth, sss;              // ring stages per warp, supersteps per stage
-  uint32_t slot_bytes, xrec_bytes;
+  uint32_t slot_bytes, xrec_bytes, hp_bytes;
   unsigned long long* trace;   // optional: per barrier and CTA (arrive, pass) in ns
 };
 
@@ -182,6 +183,32 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+// ---- flagged data ("flag in data"): every value crossing CTAs travels as an
+// 8-byte {value, flag} pair written with ONE store; the reader polls the pair
+// itself until the flag is the one of the current (launch, layer).  No fence, no
+// separate signal, no grid barrier: the hand-off costs one store plus one load
+// round trip (a grid barrier costs 1.3-1.7 us on 148 CTAs, tools/ubench/gridbar.cu).
+__device__ __forceinline__ float4 ld_pair2(const float* p) {  // two pairs: {v0, f0, v1, f1}
+  float4 v;
+  asm volatile("ld.volatile.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float2 ld_pair(const float* p) {
+  float2 v;
+  asm volatile("ld.volatile.global.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_pair(float* p, float v, uint32_t flag) {
+  asm volatile("st.volatile.global.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(v), "f"(__uint_as_float(flag))
+               : "memory");
+}
+__device__ __forceinline__ bool flags_ok(const float4& a, uint32_t fl) {
+  return __float_as_uint(a.y) == fl && __float_as_uint(a.w) == fl;
+}
+
 template <int BITS, int GPS>
 __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan pl) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -200,6 +227,7 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   const char** ltab = (const char**)(fullb + kSWarps * depth);  // [L][12]: qw[4], qsz[4], n1, n2, kc, vc
   uint32_t* ctab = (uint32_t*)(ltab + pl.L * kLtab);            // this CTA's unit ranges
   uint32_t* twob = ctab + kCtab;                                // two-CTA panel bits
+  float* hp = (float*)(twob + ((pl.two_words + 3) & ~3u));      // the residual rows of this CTA's slab
 
   static_assert(sizeof(SLayer) == kLtab * sizeof(void*), "layer table entry");
   for (int i = tid; i < pl.L * kLtab; i += kSThreads)
@@ -210,6 +238,8 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     for (int i = 0; i < kSWarps * depth; ++i) mbar_init(&fullb[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // flags of this launch: epoch * L + layer + 1 (the epoch advances at kernel exit)
+  const uint32_t fl0 = __ldcg(pl.bar + 3) * (uint32_t)pl.L + 1u;
   __syncthreads();
 
   unsigned char* ring = rings + (size_t)warp * depth * slot_bytes;
@@ -272,121 +302,132 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   }
   __syncwarp();
 
-  // ---- grid barrier -----------------------------------------------------------
-  unsigned int nbar = 0;
-  auto stamp = [&](int i) {  // trace point i of the phase ending at barrier nbar
-    if (pl.trace && tid == 0) pl.trace[((size_t)nbar * G + cta) * 4 + i] = gtime();
+  // ---- trace / waiting ----------------------------------------------------------
+  unsigned int nph = 0;  // phases done (5 per layer)
+  auto stamp = [&](int i) {  // trace point i of the current phase
+    if (pl.trace && tid == 0) pl.trace[((size_t)nph * G + cta) * 4 + i] = gtime();
   };
-  auto grid_arrive = [&]() {
-    __syncthreads();
-    if (tid == 0) {
-      if (pl.trace) pl.trace[((size_t)nbar * G + cta) * 4] = gtime();
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(pl.bar) : "memory");
+  // a poll loop gives up after 2 s (error word bit 0) instead of hanging the GPU
+  auto spin_guard = [&](uint32_t& spins, unsigned long long& t0) {
+    if ((++spins & 255u) != 0) return false;
+    if (t0 == 0) {
+      t0 = gtime();
+      return false;
     }
-    ++nbar;
-  };
-  auto grid_wait = [&]() {
-    if (tid == 0) {
-      const unsigned int target = nbar * G;
-      const unsigned long long t0 = gtime();
-      unsigned int spins = 0;
-      for (;;) {
-        unsigned int v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pl.bar) : "memory");
-        if (v >= target) break;
-        if ((++spins & 1023u) == 0 && gtime() - t0 > 2000000000ull) {
-          atomicOr(pl.bar + 1, 1u);
-          break;
-        }
-      }
-      if (pl.trace) pl.trace[((size_t)(nbar - 1) * G + cta) * 4 + 1] = gtime();
-    }
-    __syncthreads();
+    if (gtime() - t0 < 2000000000ull) return false;
+    atomicOr(pl.bar + 1, 1u);
+    return true;
   };
 
   // A column block c .. c + 3 of a phase's output lies in one panel; each K slab
   // contributed one partial (slot 2k) or two (2k + 1 too, when the panel spans
-  // two CTAs of group k; host-built bit table).  All loads of a sum are issued
-  // before the adds.
-  auto slot_sum4 = [&](int ph, uint32_t c) {
-    const uint32_t p = c >> 4, st = pl.pstride[ph];
+  // two CTAs of group k; host-built bit table), as {value, flag} pairs in the
+  // buffer set `bs` (layer % 3).  Polls until every pair carries flag fl; the
+  // slots are added in a fixed order.  Called by whole warps.
+  auto slot_sum4 = [&](int ph, uint32_t c, uint32_t fl, int bs) {
+    const uint32_t p = c >> 4;
+    const size_t st = (size_t)pl.pstride[ph] * 2;
     const uint32_t* tb = twob + pl.two_off[ph] + (p >> 5);
-    const float* src = pl.part[ph] + c;
     const int ksl = pl.ksl[ph];
-    float4 a[kMaxKsl], b[kMaxKsl];
+    const float* src = pl.part[ph] + (size_t)bs * (2 * ksl) * st + (size_t)c * 2;
+    float4 r;
+    uint32_t spins = 0;
+    unsigned long long t0 = 0;
+    for (;;) {
+      bool ok = true;
+      r = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < kMaxKsl; ++k) {
-      const bool on = k < ksl;
-      const bool two = on && ((tb[k * pl.two_wp[ph]] >> (p & 31)) & 1u);
-      a[k] = on ? ldcg4(src + (size_t)(2 * k) * st) : make_float4(0.f, 0.f, 0.f, 0.f);
-      b[k] = two ? ldcg4(src + (size_t)(2 * k + 1) * st) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    float4 r = a[0];
-    add4(r, b[0]);
-#pragma unroll
-    for (int k = 1; k < kMaxKsl; ++k) {
-      add4(r, a[k]);
-      add4(r, b[k]);
+      for (int k = 0; k < kMaxKsl; ++k) {
+        if (k < ksl) {
+          const bool two = (tb[k * pl.two_wp[ph]] >> (p & 31)) & 1u;
+          const float4 x0 = ld_pair2(src + (size_t)(2 * k) * st), x1 = ld_pair2(src + (size_t)(2 * k) * st + 4);
+          float4 y0 = make_float4(0.f, __uint_as_float(fl), 0.f, __uint_as_float(fl)), y1 = y0;
+          if (two) {
+            y0 = ld_pair2(src + (size_t)(2 * k + 1) * st);
+            y1 = ld_pair2(src + (size_t)(2 * k + 1) * st + 4);
+          }
+          ok = ok && flags_ok(x0, fl) && flags_ok(x1, fl) && flags_ok(y0, fl) && flags_ok(y1, fl);
+          r.x += x0.x; r.y += x0.z; r.z += x1.x; r.w += x1.z;
+          r.x += y0.x; r.y += y0.z; r.z += y1.x; r.w += y1.z;
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
+      if (spin_guard(spins, t0)) break;
     }
     return r;
   };
-  auto slot_sum1 = [&](int ph, uint32_t c) {  // one column
-    const uint32_t p = c >> 4, st = pl.pstride[ph];
+  auto slot_sum1 = [&](int ph, uint32_t c, uint32_t fl, int bs) {  // one column
+    const uint32_t p = c >> 4;
+    const size_t st = (size_t)pl.pstride[ph] * 2;
     const uint32_t* tb = twob + pl.two_off[ph] + (p >> 5);
-    const float* src = pl.part[ph] + c;
     const int ksl = pl.ksl[ph];
-    float a[kMaxKsl], b[kMaxKsl];
+    const float* src = pl.part[ph] + (size_t)bs * (2 * ksl) * st + (size_t)c * 2;
+    float r;
+    uint32_t spins = 0;
+    unsigned long long t0 = 0;
+    for (;;) {
+      bool ok = true;
+      r = 0.f;
 #pragma unroll
-    for (int k = 0; k < kMaxKsl; ++k) {
-      const bool on = k < ksl;
-      const bool two = on && ((tb[k * pl.two_wp[ph]] >> (p & 31)) & 1u);
-      a[k] = on ? __ldcg(src + (size_t)(2 * k) * st) : 0.f;
-      b[k] = two ? __ldcg(src + (size_t)(2 * k + 1) * st) : 0.f;
+      for (int k = 0; k < kMaxKsl; ++k) {
+        if (k < ksl) {
+          const bool two = (tb[k * pl.two_wp[ph]] >> (p & 31)) & 1u;
+          const float2 x = ld_pair(src + (size_t)(2 * k) * st);
+          float2 y = make_float2(0.f, __uint_as_float(fl));
+          if (two) y = ld_pair(src + (size_t)(2 * k + 1) * st);
+          ok = ok && __float_as_uint(x.y) == fl && __float_as_uint(y.y) == fl;
+          r += x.x;
+          r += y.x;
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
+      if (spin_guard(spins, t0)) break;
     }
-    float r = a[0] + b[0];
-#pragma unroll
-    for (int k = 1; k < kMaxKsl; ++k) r += a[k] + b[k];
     return r;
   };
   // 1 / rms of a residual from the per-slab sums of squares its prologue (of
-  // phase 0: norm1, phase 2: norm2) published
-  auto rinv_of = [&](int which) {
-    float ssum = 0.f;
+  // phase 0: norm1, phase 2: norm2) published for this layer.  Whole warps.
+  auto rinv_of = [&](int which, uint32_t fl, int bs) {
+    const float* src = pl.ssq + ((size_t)bs * 2 + which) * kMaxKsl * 2;
+    float ssum;
+    uint32_t spins = 0;
+    unsigned long long t0 = 0;
+    for (;;) {
+      bool ok = true;
+      ssum = 0.f;
 #pragma unroll
-    for (int k = 0; k < kMaxKsl; ++k)
-      if (k < pl.ksl[2 * which]) ssum += __ldcg(pl.ssq + which * kMaxKsl + k);
+      for (int k = 0; k < kMaxKsl; ++k)
+        if (k < pl.ksl[2 * which]) {
+          const float2 x = ld_pair(src + 2 * k);
+          ok = ok && __float_as_uint(x.y) == fl;
+          ssum += x.x;
+        }
+      if (__all_sync(0xffffffffu, ok)) break;
+      if (spin_guard(spins, t0)) break;
+    }
     return rsqrtf(ssum / (float)pl.d + pl.eps);
   };
 
   // Digitise this CTA's K slab of a phase's input into the shared-memory
   // records: item it = rows 4 it .. 4 it + 3 (absolute), record of local
   // superstep (it >> 6) - s0.  load(it) fetches the item's inputs (addresses
-  // clamped into the vector), finish(it, raw, v) turns them into the four
-  // values (zeros beyond K); UB items per thread are loaded before any is
-  // finished.
-  auto digitize_rows = [&](int ph, auto ub_c, auto&& load, auto&& finish) {
-    constexpr int UB = decltype(ub_c)::value;
+  // clamped into the vector; it may poll), finish(it, raw, v) turns them into
+  // the four values (zeros beyond K).
+  auto digitize_rows = [&](int ph, auto&& load, auto&& finish) {
     const uint32_t umask = IPU == 32 ? 0xffffffffu : ((1u << IPU) - 1u) << (lane & ~(IPU - 1));
     const int s0 = (int)ctab[ph * kCrow + 34], sk = (int)ctab[ph * kCrow + 35];
     const int itb = s0 * 64, nit = itb + sk * 64;
-    for (int it0 = itb + warp * 32; it0 < nit; it0 += kSThreads * UB) {
-      decltype(load(0)) r[UB];
-#pragma unroll
-      for (int u = 0; u < UB; ++u) r[u] = load(min(it0 + u * kSThreads + lane, nit - 1));
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        if (it0 + u * kSThreads < nit) {
-          const int it = it0 + u * kSThreads + lane;
-          float v[4];
-          finish(it, r[u], v);
-          const Digits dg = digitize<IPU>(v, umask);
-          unsigned char* rec = xrec + (size_t)((it >> 6) - s0) * kSRec;
-          store_digits((uint32_t*)rec, (it >> 3) & 7, 0, 1, it & 7, dg);
-          if ((it % IPU) == 0)
-            ((float4*)(rec + kSRecDig))[(it & 63) / IPU] =
-                make_float4(dg.scale * 65536.f, dg.xsum * dg.scale, dg.scale, 0.f);
-        }
-      }
+    for (int it0 = itb + warp * 32; it0 < nit; it0 += kSThreads) {
+      const int it = it0 + lane;
+      const auto r = load(it);
+      float v[4];
+      finish(it, r, v);
+      const Digits dg = digitize<IPU>(v, umask);
+      unsigned char* rec = xrec + (size_t)((it >> 6) - s0) * kSRec;
+      store_digits((uint32_t*)rec, (it >> 3) & 7, 0, 1, it & 7, dg);
+      if ((it % IPU) == 0)
+        ((float4*)(rec + kSRecDig))[(it & 63) / IPU] =
+            make_float4(dg.scale * 65536.f, dg.xsum * dg.scale, dg.scale, 0.f);
     }
   };
   // block sum of a per-thread value (ends with a CTA barrier: also publishes
@@ -405,7 +446,7 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   // ---- one GEMV phase: consume this warp's unit range ----------------------------
   int wslot = 0;
   uint32_t wph = 0;
-  auto gemv_phase = [&](int ph) {
+  auto gemv_phase = [&](int ph, uint32_t fl, int bs) {
     const uint32_t* row = ctab + ph * kCrow;
     const uint32_t Sk = row[35];
     const uint32_t lo = row[warp], hi = row[warp + 1];
@@ -455,6 +496,7 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     // the CTA's partial of every panel it touched: its warps' segments in warp
     // order; slot 2 slab (+ 1 when the panel started in the previous CTA)
     const uint32_t LO = row[0], HI = row[16], pf = row[17], npan = row[33];
+    float* dst = pl.part[ph] + (size_t)bs * (2 * pl.ksl[ph]) * pl.pstride[ph] * 2;
     for (uint32_t idx = tid; idx < npan * 16; idx += kSThreads) {
       const uint32_t pp = pf + idx / 16, col = idx % 16;
       const uint32_t ua = max(LO, pp * Sk), ub = min(HI, (pp + 1) * Sk) - 1;
@@ -466,9 +508,10 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           acc += wpart[((uint32_t)w * kMaxSeg + (pp - row[17 + w])) * 16 + col];
       }
       const uint32_t sl = 2 * row[36] + (pp * Sk < LO ? 1u : 0u);
-      pl.part[ph][(size_t)sl * pl.pstride[ph] + pp * 16 + col] = acc;
+      st_pair(dst + ((size_t)sl * pl.pstride[ph] + pp * 16 + col) * 2, acc, fl);
     }
-    grid_arrive();
+    stamp(0);
+    ++nph;
   };
 
   // The cached K / V rows this CTA will read in the attention phase of layer l
@@ -493,35 +536,12 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   // position, taken from shared memory by warp 0 of the last chunk's CTA (which
   // also appends it to the cache).  The first batch of cached K / V rows of each
   // warp (first head of the CTA) and the RoPE factors are loaded into registers
-  // BEFORE the grid barrier of the QKV phase is awaited.
+  // before the QKV outputs are awaited.
   constexpr int NB = 8;
-  uint2 kr0[NB], vr0[NB];
-  float rope_c = 0.f, rope_s = 0.f;
-  auto attention_preload = [&](int l) {
-    const int cph = pl.cph, ngroups = (int)G / cph;
-    const int gi = (int)cta / cph, j = (int)cta % cph;
-    const int Lc = (pl.pos + cph - 1) / cph;
-    const int p0 = j * Lc, p1 = min(p0 + Lc, pl.pos);
-    if (gi >= ngroups || gi >= pl.H) return;
-    if (tid < kHD / 2) {
-      rope_c = pl.cosv[tid];
-      rope_s = pl.sinv[tid];
-    }
-    const __half* kb = (const __half*)ltab[l * kLtab + 10] + (size_t)gi * pl.ctx * kHD + 4 * lane;
-    const __half* vb = (const __half*)ltab[l * kLtab + 11] + (size_t)gi * pl.ctx * kHD + 4 * lane;
-#pragma unroll
-    for (int u = 0; u < NB; ++u) {
-      const int pu = p0 + warp + kSWarps * u;
-      if (pu < p1) {
-        kr0[u] = __ldcg((const uint2*)(kb + (size_t)pu * kHD));
-        vr0[u] = __ldcg((const uint2*)(vb + (size_t)pu * kHD));
-      }
-    }
-  };
-  auto attention = [&](int l) {
+  auto attention = [&](int l, uint32_t fl, int bs) {
     float* qs = (float*)xrec;       // rotated q (through f16)
     float* raw = qs + kHD;          // [3][128]: q, k, v of the new token (k, v: as cached)
-    float* wsm = raw + 3 * kHD;     // [warp][kAttRow]
+    float* wsm = raw + 3 * kHD;     // [warp][kAttSm]
     __half* const kc = (__half*)ltab[l * kLtab + 10];
     __half* const vc = (__half*)ltab[l * kLtab + 11];
     const int cph = pl.cph, ngroups = (int)G / cph;
@@ -529,11 +549,30 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     const int Lc = (pl.pos + cph - 1) / cph;
     const int p0 = j * Lc, p1 = min(p0 + Lc, pl.pos);  // cached rows of this chunk
     const bool mine = j == cph - 1;                    // this CTA takes the new token
-    if (gi < ngroups) {
-      const float rinv = rinv_of(0);
+    float* const attp = pl.attp + (size_t)bs * pl.H * cph * kAttRow;
+    if (gi < ngroups && gi < pl.H) {
+      uint2 kr0[NB], vr0[NB];
+      float rope_c = 0.f, rope_s = 0.f;
+      if (tid < kHD / 2) {
+        rope_c = pl.cosv[tid];
+        rope_s = pl.sinv[tid];
+      }
+      {
+        const __half* kb = kc + (size_t)gi * pl.ctx * kHD + 4 * lane;
+        const __half* vb = vc + (size_t)gi * pl.ctx * kHD + 4 * lane;
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int pu = p0 + warp + kSWarps * u;
+          if (pu < p1) {
+            kr0[u] = __ldcg((const uint2*)(kb + (size_t)pu * kHD));
+            vr0[u] = __ldcg((const uint2*)(vb + (size_t)pu * kHD));
+          }
+        }
+      }
+      const float rinv = rinv_of(0, fl, bs);
       for (int hh = gi; hh < pl.H; hh += ngroups) {
         if (tid < 3 * kHD && (tid < kHD || mine))
-          raw[tid] = slot_sum1(0, (uint32_t)(tid >> 7) * pl.d + (uint32_t)hh * kHD + (tid & 127)) * rinv;
+          raw[tid] = slot_sum1(0, (uint32_t)(tid >> 7) * pl.d + (uint32_t)hh * kHD + (tid & 127), fl, bs) * rinv;
         __syncthreads();
         float k0 = 0.f, k1 = 0.f, v0 = 0.f, v1 = 0.f;
         if (tid < kHD / 2) {
@@ -640,75 +679,74 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           m = mb;
         }
         stamp(3);
-        *(float4*)(wsm + warp * kAttRow + 4 * lane) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *(float4*)(wsm + warp * kAttSm + 4 * lane) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         if (lane == 0) {
-          wsm[warp * kAttRow + kHD] = m;
-          wsm[warp * kAttRow + kHD + 1] = ls;
+          wsm[warp * kAttSm + kHD] = m;
+          wsm[warp * kAttSm + kHD + 1] = ls;
         }
         __syncthreads();
         if (tid < kHD) {  // combine the warps in warp order
           float M = -INFINITY;
 #pragma unroll
-          for (int w = 0; w < kSWarps; ++w) M = fmaxf(M, wsm[w * kAttRow + kHD]);
+          for (int w = 0; w < kSWarps; ++w) M = fmaxf(M, wsm[w * kAttSm + kHD]);
           float o = 0.f, Ls = 0.f;
 #pragma unroll
           for (int w = 0; w < kSWarps; ++w) {
-            const float mw = wsm[w * kAttRow + kHD];
+            const float mw = wsm[w * kAttSm + kHD];
             const float wt = mw == -INFINITY ? 0.f : __expf(mw - M);
-            o = fmaf(wt, wsm[w * kAttRow + tid], o);
-            Ls = fmaf(wt, wsm[w * kAttRow + kHD + 1], Ls);
+            o = fmaf(wt, wsm[w * kAttSm + tid], o);
+            Ls = fmaf(wt, wsm[w * kAttSm + kHD + 1], Ls);
           }
-          float* dst = pl.attp + ((size_t)hh * cph + j) * kAttRow;
-          dst[tid] = o;
+          // partial of (head, chunk) as {value, flag} pairs: acc[128], m, l
+          float* dst = attp + ((size_t)hh * cph + j) * kAttRow;
+          st_pair(dst + 2 * tid, o, fl);
           if (tid == 0) {
-            dst[kHD] = M;
-            dst[kHD + 1] = Ls;
+            st_pair(dst + 2 * kHD, M, fl);
+            st_pair(dst + 2 * kHD + 2, Ls, fl);
           }
         }
         __syncthreads();
       }
     }
-    grid_arrive();
+    stamp(0);
+    ++nph;
   };
 
   // ---- the step ------------------------------------------------------------------------
   const int d = pl.d;
-  // Residual prologue of an RMSNorm'd GEMV over this CTA's slab of rows:
-  // a = hsrc (+ the partial slots of phase pph); the CTA's share of a is stored
-  // to hdst; a * nw is digitised; the slab's sum of squares goes to ssq[which]
-  // (applied as 1 / rms by the GEMV's consumer).
+  // Residual prologue of an RMSNorm'd GEMV over this CTA's slab of rows (the
+  // same slab in phases 0 and 2; the CTA keeps those rows of the residual in
+  // shared memory, hp): hp += the partial slots of phase pph (flag pfl, buffer
+  // set pbs); hp * nw is digitised; the slab's sum of squares is published as
+  // ssq[which] (applied as 1 / rms by the GEMV's consumer).
   struct ResRaw {
     float4 h, w, p;
   };
-  auto residual_prologue = [&](int ph, const float* hsrc, int pph, float* hdst, const float* nw,
-                               int which) {
+  auto residual_prologue = [&](int ph, int pph, uint32_t pfl, int pbs, const float* nw, int which,
+                               uint32_t fl, int bs) {
     float ss = 0.f;
-    const uint32_t own_q = pl.own_q[ph];
-    const uint32_t own0 = ctab[ph * kCrow + 34] * 64 + ctab[ph * kCrow + 37] * own_q;  // this CTA's items
+    const int itb = (int)ctab[ph * kCrow + 34] * 64;
     digitize_rows(
-        ph, std::integral_constant<int, 1>{},
+        ph,
         [&](int it) {
           ResRaw r;
           const uint32_t c = min(4u * it, (uint32_t)d - 4u);
-          r.h = ldcg4(hsrc + c);
+          r.h = pph >= 0 ? *(const float4*)(hp + 4 * (it - itb)) : ldcg4(pl.h_in + c);
           r.w = __ldg((const float4*)(nw + c));
-          r.p = pph >= 0 ? slot_sum4(pph, c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          r.p = pph >= 0 ? slot_sum4(pph, c, pfl, pbs) : make_float4(0.f, 0.f, 0.f, 0.f);
           return r;
         },
         [&](int it, const ResRaw& r, float (&v)[4]) {
-          const uint32_t c = 4u * it;
-          if ((int)c < d) {
-            float4 a = r.h;
-            add4(a, r.p);
-            if ((uint32_t)it - own0 < own_q) *(float4*)(hdst + c) = a;
-            ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
-            v[0] = a.x * r.w.x; v[1] = a.y * r.w.y; v[2] = a.z * r.w.z; v[3] = a.w * r.w.w;
-          } else {
-            v[0] = v[1] = v[2] = v[3] = 0.f;
-          }
+          float4 a = r.h;
+          add4(a, r.p);
+          if (4 * it >= d) a = make_float4(0.f, 0.f, 0.f, 0.f);
+          *(float4*)(hp + 4 * (it - itb)) = a;
+          ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+          v[0] = a.x * r.w.x; v[1] = a.y * r.w.y; v[2] = a.z * r.w.z; v[3] = a.w * r.w.w;
         });
     ss = block_sum(ss);
-    if (ctab[ph * kCrow + 37] == 0 && tid == 0) pl.ssq[which * kMaxKsl + ctab[ph * kCrow + 36]] = ss;
+    if (ctab[ph * kCrow + 37] == 0 && tid == 0)
+      st_pair(pl.ssq + (((size_t)bs * 2 + which) * kMaxKsl + ctab[ph * kCrow + 36]) * 2, ss, fl);
   };
   struct AttRaw {
     float4 a[kMaxCph];
@@ -720,26 +758,40 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   for (int l = 0; l < pl.L; ++l) {
     const float* const n1 = (const float*)ltab[l * kLtab + 8];
     const float* const n2 = (const float*)ltab[l * kLtab + 9];
+    const uint32_t fl = fl0 + (uint32_t)l;  // this layer's flag
+    const int bs = l % 3;                   // and buffer set
 #pragma unroll 1
     for (int st = 0; st < 4; ++st) {  // one call site of the GEMV loop (code size)
       if (st == 0) {
         // QKV: h (layer input) = h' of the previous layer + its down_proj partials
-        residual_prologue(0, l == 0 ? pl.h_in : pl.hx, l == 0 ? -1 : 3, pl.hy, n1, 0);
+        residual_prologue(0, l == 0 ? -1 : 3, fl - 1u, (l + 2) % 3, n1, 0, fl, bs);
         prefetch_kv(l);
       } else if (st == 1) {
         // o_proj: combine the attention partials of each head
         const int cph = pl.cph;
+        const float* const attp = pl.attp + (size_t)bs * pl.H * cph * kAttRow;
         digitize_rows(
-            1, std::integral_constant<int, 1>{},
+            1,
             [&](int it) {
               AttRaw r;
               const uint32_t c = min(4u * it, (uint32_t)d - 4u);
-              const float* src = pl.attp + (size_t)(c / kHD) * cph * kAttRow;
+              const float* src = attp + (size_t)(c / kHD) * cph * kAttRow;
+              uint32_t spins = 0;
+              unsigned long long t0 = 0;
+              for (;;) {
+                bool ok = true;
 #pragma unroll
-              for (int j = 0; j < kMaxCph; ++j) {
-                const int jj = min(j, cph - 1);
-                r.a[j] = ldcg4(src + jj * kAttRow + (c % kHD));
-                r.ml[j] = __ldcg((const float2*)(src + jj * kAttRow + kHD));
+                for (int j = 0; j < kMaxCph; ++j) {
+                  const int jj = min(j, cph - 1);
+                  const float4 x0 = ld_pair2(src + jj * kAttRow + 2 * (c % kHD));
+                  const float4 x1 = ld_pair2(src + jj * kAttRow + 2 * (c % kHD) + 4);
+                  const float4 z = ld_pair2(src + jj * kAttRow + 2 * kHD);
+                  ok = ok && flags_ok(x0, fl) && flags_ok(x1, fl) && flags_ok(z, fl);
+                  r.a[j] = make_float4(x0.x, x0.z, x1.x, x1.z);
+                  r.ml[j] = make_float2(z.x, z.z);
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+                if (spin_guard(spins, t0)) break;
               }
               return r;
             },
@@ -765,18 +817,18 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
         __syncthreads();
       } else if (st == 2) {
         // gate|up: h' = h + o_proj partials
-        residual_prologue(2, pl.hy, 1, pl.hx, n2, 1);
+        residual_prologue(2, 1, fl, bs, n2, 1, fl, bs);
       } else {
         // down_proj: SwiGLU of the gate|up partials (x 1 / rms)
         const int ffn = pl.ffn;
-        const float rinv2 = rinv_of(1);
+        const float rinv2 = rinv_of(1, fl, bs);
         digitize_rows(
-            3, std::integral_constant<int, 1>{},
+            3,
             [&](int it) {
               GuRaw r;
               const uint32_t c = min(4u * it, (uint32_t)ffn - 4u);
-              r.g = slot_sum4(2, c);
-              r.u = slot_sum4(2, (uint32_t)ffn + c);
+              r.g = slot_sum4(2, c, fl, bs);
+              r.u = slot_sum4(2, (uint32_t)ffn + c, fl, bs);
               return r;
             },
             [&](int it, const GuRaw& r, float (&v)[4]) {
@@ -792,32 +844,48 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
         __syncthreads();
       }
       stamp(2);
-      gemv_phase(st);
-      if (st == 0) attention_preload(l);
-      grid_wait();
-      if (st == 0) {
-        attention(l);
-        grid_wait();
+      gemv_phase(st, fl, bs);
+      if (st == 0) attention(l, fl, bs);
+    }
+    // Skew bound for the three buffer sets: this CTA enters layer l + 1 (whose
+    // writes reuse the buffers of layer l - 2, last read early in layer l - 1)
+    // only after every CTA has finished layer l - 1.  Normally long satisfied.
+    if (tid == 0) {
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(pl.bar) : "memory");
+      if (l >= 1) {
+        const unsigned int target = (unsigned int)l * G;
+        uint32_t spins = 0;
+        unsigned long long t0 = 0;
+        for (;;) {
+          unsigned int v;
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pl.bar) : "memory");
+          if (v >= target) break;
+          if (spin_guard(spins, t0)) break;
+        }
       }
     }
   }
-  // the step's output: h' of the last layer + its down_proj partials (each CTA
-  // its share of its slab's rows)
+  // the step's output: the residual + the last layer's down_proj partials (each
+  // CTA its share of its slab's rows)
   {
-    const uint32_t own0 = ctab[34] * 64 + ctab[37] * pl.own_q[0];
-    const uint32_t own1 = min(own0 + pl.own_q[0], min((ctab[34] + ctab[35]) * 64, (uint32_t)d / 4));
-    for (uint32_t it = own0 + tid; it < own1; it += kSThreads) {
-      float4 a = ldcg4(pl.hx + 4 * it);
-      add4(a, slot_sum4(3, 4 * it));
-      *(float4*)(pl.h_out + 4 * it) = a;
+    const uint32_t itb = ctab[34] * 64, nit = min((ctab[34] + ctab[35]) * 64, (uint32_t)d / 4);
+    const uint32_t own0 = itb + ctab[37] * pl.own_q[0];
+    const uint32_t own1 = min(own0 + pl.own_q[0], nit);
+    const uint32_t fl = fl0 + (uint32_t)pl.L - 1u;
+    for (uint32_t it0 = own0 + warp * 32; it0 < own1; it0 += kSThreads) {  // whole warps poll
+      const uint32_t it = min(it0 + lane, nit - 1);
+      float4 a = *(const float4*)(hp + 4 * (it - itb));
+      add4(a, slot_sum4(3, 4 * it, fl, (pl.L - 1) % 3));
+      if (it0 + lane < own1) *(float4*)(pl.h_out + 4 * it) = a;
     }
   }
-  // re-arm the barrier for the next launch: the last CTA to leave resets it
+  // the last CTA to leave re-arms the counters and advances the launch epoch
   __syncthreads();
   if (tid == 0) {
     if (atomicAdd(pl.bar + 2, 1u) == G - 1) {
       pl.bar[0] = 0u;
       pl.bar[2] = 0u;
+      pl.bar[3] = pl.bar[3] + 1u;
       __threadfence();
     }
   }
@@ -924,14 +992,19 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   const int want[4] = {g_stack_ksl / 1000 % 10, g_stack_ksl / 100 % 10, g_stack_ksl / 10 % 10,
                        g_stack_ksl % 10};
   for (int ph = 0; ph < 4; ++ph) {
-    const uint32_t P = pl.P[ph], S = pl.S[ph];
-    int ksl = 1;
+    pl.ksl[ph] = 1;
     for (int k : {4, 2})
-      if (k <= want[ph] && G % k == 0 && S >= (uint32_t)k && P >= (uint32_t)(G / k)) {
-        ksl = k;
+      if (k <= want[ph] && G % k == 0 && pl.S[ph] >= (uint32_t)k && pl.P[ph] >= (uint32_t)(G / k)) {
+        pl.ksl[ph] = k;
         break;
       }
-    pl.ksl[ph] = ksl;
+  }
+  // QKV and gate|up read the same residual rows: one slab split for both (the
+  // CTA keeps its slab of the residual in shared memory)
+  pl.ksl[0] = pl.ksl[2] = std::min(pl.ksl[0], pl.ksl[2]);
+  for (int ph = 0; ph < 4; ++ph) {
+    const uint32_t P = pl.P[ph], S = pl.S[ph];
+    const int ksl = pl.ksl[ph];
     const int GJ = G / ksl;
     const uint32_t GWJ = (uint32_t)GJ * kSWarps;  // warps per slab group
     pl.own_q[ph] = (uint32_t)(((S + ksl - 1) / ksl * 64 + GJ - 1) / GJ);
@@ -975,8 +1048,11 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   const int gps = (int)(256 / e.group_size);
   int sss = g_stack_sss, depth = 0;
   size_t slot = 0;
+  const size_t hp_bytes = (size_t)((pl.S[0] + pl.ksl[0] - 1) / pl.ksl[0]) * kSuper * 4;
+  pl.hp_bytes = (uint32_t)hp_bytes;
   const size_t fixed = xrec_al + kSWarps * kMaxSeg * 16 * 4 + 32 * 4 +
-                       (size_t)e.layers * kLtab * sizeof(void*) + kCtab * 4 + two.size() * 4;
+                       (size_t)e.layers * kLtab * sizeof(void*) + kCtab * 4 +
+                       ((two.size() + 3) & ~(size_t)3) * 4 + hp_bytes;
   const size_t budget = 227 * 1024;
   for (; sss >= 1; --sss) {  // 2-superstep stages unless only 1-superstep ones fit
     slot = (size_t)sss * (e.bits * 512 + gps * 128);
@@ -1001,10 +1077,10 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   };
   const size_t o_lay = take((size_t)e.layers * sizeof(SLayer));
   size_t o_part[4];
-  for (int ph = 0; ph < 4; ++ph) o_part[ph] = take((size_t)2 * pl.ksl[ph] * pl.pstride[ph] * 4);
-  const size_t o_att = take((size_t)e.heads * pl.cph * kAttRow * 4);
-  const size_t o_hx = take((size_t)e.d_model * 4), o_hy = take((size_t)e.d_model * 4);
-  const size_t o_bar = take(256), o_ssq = take(2 * kMaxKsl * 4);
+  for (int ph = 0; ph < 4; ++ph)
+    o_part[ph] = take((size_t)3 * 2 * pl.ksl[ph] * pl.pstride[ph] * 2 * 4);
+  const size_t o_att = take((size_t)3 * e.heads * pl.cph * kAttRow * 4);
+  const size_t o_bar = take(256), o_ssq = take((size_t)3 * 2 * kMaxKsl * 2 * 4);
   const size_t o_ctab = take(ctab.size() * 4), o_two = take(two.size() * 4);
   std::vector<SLayer> tab(e.layers);
   for (int l = 0; l < e.layers; ++l) {
@@ -1035,8 +1111,6 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   pl.layers = (const SLayer*)(b + o_lay);
   for (int ph = 0; ph < 4; ++ph) pl.part[ph] = (float*)(b + o_part[ph]);
   pl.attp = (float*)(b + o_att);
-  pl.hx = (float*)(b + o_hx);
-  pl.hy = (float*)(b + o_hy);
   pl.bar = (unsigned int*)(b + o_bar);
   pl.ssq = (float*)(b + o_ssq);
   pl.ctab = (const uint32_t*)(b + o_ctab);

@@ -56,29 +56,29 @@ torch.cuda.synchronize()
 Lb.qigen_debug_trace(None)
 assert m.stack_error() == 0
 t = buf.cpu().numpy().reshape(nbar, G, 4).astype(np.float64) / 1e3
-t0 = t[0, :, 0].min()
+t0 = t[0, :, 2].min()
 names = ["qkv", "attn", "o", "gu", "down"]
-prev_pass = None
+# stamps per phase and CTA: [0] outputs stored, [2] prologue done (attention: q ready),
+# [3] GEMV loop done (attention: KV loop done); all relative to the previous phase's last store
 tot = {}
+prev = 0.0
 for b in range(nbar):
-    arr, pas = t[b, :, 0] - t0, t[b, :, 1] - t0
     ph = names[b % 5]
-    work = arr.max() - (prev_pass if prev_pass is not None else 0.0)
-    lat = pas.max() - arr.max()
-    base = prev_pass if prev_pass is not None else 0.0
-    pro = (t[b, :, 2] - t0).max() - base   # prologue done (last CTA); attention: q ready
-    loop = (t[b, :, 3] - t0).max() - base  # GEMV loop done (last CTA); attention: KV loop done (warp 0)
-    tot.setdefault(ph, []).append((work, lat, arr.max() - arr.min(), pro, loop))
+    end = t[b, :, 0] - t0
+    live = t[b, :, 2] > 0  # CTAs that took part (attention: idle CTAs have no stamp)
+    pro = (t[b, live, 2] - t0).max() - prev
+    loop = (t[b, live, 3] - t0).max() - prev
+    work = end.max() - prev
+    tot.setdefault(ph, []).append((work, pro, loop, end.max() - end[live].min()))
     if b < 10 or b >= nbar - 5:
-        print(f"L{b // 5} {ph:5s} arrive {arr.min():8.2f}-{arr.max():8.2f} (spread {arr.max() - arr.min():5.2f})"
-              f"  pass {pas.min():8.2f}-{pas.max():8.2f}  phase {work:6.2f}  barrier {lat:5.2f}")
-    prev_pass = pas.max()
-print("mean per phase (us): phase time (pass of previous barrier -> last arrival), barrier latency, "
-      "arrival spread, prologue done, GEMV loop done (both since the previous barrier)")
+        print(f"L{b // 5} {ph:5s} stored {end[live].min():8.2f}-{end.max():8.2f}  phase {work:6.2f}  "
+              f"prologue {pro:5.2f}  loop done {loop:5.2f}")
+    prev = end.max()
+print("mean per phase (us, since the previous phase's last store): phase, prologue done, loop done, "
+      "spread of the stores")
 s_all = 0.0
 for ph in names:
     a = np.array(tot[ph])
-    s_all += a[:, 0].mean() + a[:, 1].mean()
-    print(f"  {ph:5s} {a[:, 0].mean():6.2f} {a[:, 1].mean():5.2f} {a[:, 2].mean():5.2f} "
-          f"{a[:, 3].mean():6.2f} {a[:, 4].mean():6.2f}")
+    s_all += a[:, 0].mean()
+    print(f"  {ph:5s} {a[:, 0].mean():6.2f} {a[:, 1].mean():6.2f} {a[:, 2].mean():6.2f} {a[:, 3].mean():5.2f}")
 print(f"  layer total {s_all:.2f} us")
