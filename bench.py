@@ -542,6 +542,14 @@ def measure_decode(workload, B, ctx, layers, steps, warmup, tp_shard=0):
     peak, peak_src = measured_peak()
     gbs = nbytes / (ms_step / 1e3) / 1e9
     comm = getattr(model, "comm_kind", None)
+    if getattr(model, "stack", None) is not None:
+        if model.stack_error():
+            raise RuntimeError("decode stack: a wait inside the persistent kernel timed out")
+        engine = ("persistent decode stack: all layers in one cooperative launch "
+                  "(csrc/decode_stack.cu)")
+    else:
+        engine = ("per-op kernel chain (digit epilogues)" if getattr(model, "chained", False)
+                  else "per-op kernels")
     res = {
         "value": round(B / (ms_step / 1e3), 2), "unit": "tokens/s",
         "ms_per_step": round(ms_step, 4), "steps": steps,
@@ -550,7 +558,7 @@ def measure_decode(workload, B, ctx, layers, steps, warmup, tp_shard=0):
                    "ctx": ctx, "setup_s": round(setup_s, 1),
                    "parallelism": (f"tp{tp_shard} shard of rank 0 on one GPU, collectives "
                                    f"skipped (per-GPU compute only)") if tp_shard > 1
-                   else f"tp{world}", "allreduce": comm},
+                   else f"tp{world}", "allreduce": comm, "engine": engine},
         "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": round(gbs / peak, 4),
                      "bytes_per_step_per_gpu": nbytes, "traffic": None},

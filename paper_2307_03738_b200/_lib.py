@@ -129,6 +129,7 @@ SIGNATURES = {
                                        ctypes.POINTER(_I32)]),
     "qigen_decode_stack_destroy": (_I32, [_P]),
     "qigen_debug_stack_tuning": (_I32, [_I32, _I32, _I32]),
+    "qigen_debug_stack_mode": (_I32, [_I32]),
     "qigen_weights_create": (_I32, [_P, _I32, _I64, _I64, _I32, _I64, _I64, _I64, _P, _I64,
                                     _P, _P, _P, ctypes.POINTER(_P)]),
     "qigen_weights_destroy": (_I32, [_P]),

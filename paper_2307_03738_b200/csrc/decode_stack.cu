@@ -88,6 +88,7 @@ struct SPlan {
   uint32_t two_off[4], two_wp[4], two_words;  // per phase: word offset, words per slab
   float* ssq;                  // [3][2][kMaxKsl] {value, flag}: per-slab sums of squares (norm1, norm2 input)
   uint32_t own_q[4];           // residual items (4 floats) each CTA of a slab group stores
+  uint32_t pf_units[4];        // units of a phase each warp prefetches into L2 one phase ahead
   unsigned int* bar;           // [0] layers finished (all CTAs), [1] error word, [2] exit counter,
                                // [3] launch epoch
   const float* h_in;
@@ -97,6 +98,7 @@ struct SPlan {
   int pos;
   float scale, eps;
   int depth, sss;              // ring stages per warp, supersteps per stage
+  int mode;                    // tuning: 1 = stream the weights without the math
   uint32_t slot_bytes, xrec_bytes, hp_bytes;
   unsigned long long* trace;   // optional: per barrier and CTA (arrive, pass) in ns
 };
@@ -164,6 +166,7 @@ __device__ __forceinline__ void add4(float4& a, const float4 b) {
 
 __device__ __forceinline__ bool mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
+#pragma unroll 1
   for (int i = 0; i < 300; ++i) {  // x 10 ms suspend hint
     uint32_t done = 0;
     asm volatile(
@@ -214,7 +217,10 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int WB = BITS * 512, ZB = GPS * 128;
   constexpr int UPS = GPS > 2 ? GPS : 2, IPU = 64 / UPS;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // (the shuffle tells the compiler the warp index is warp-uniform: the issue
+  // cursor below then lives in uniform registers)
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const uint32_t cta = blockIdx.x, G = (uint32_t)pl.G;
   const int depth = pl.depth, sss = pl.sss;
   const uint32_t slot_bytes = pl.slot_bytes;
@@ -245,9 +251,10 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
   unsigned char* ring = rings + (size_t)warp * depth * slot_bytes;
   uint64_t* full = fullb + warp * depth;
 
-  // ---- issue cursor (lane 0): the warp's static stream of weight stages over
-  // all phases of all layers.  Units are slab-local: unit u = (panel p, local
-  // superstep u - p Sk); the weights of panel p start S supersteps apart.
+  // ---- issue cursor: the warp's static stream of weight stages over all phases
+  // of all layers, kept identically by every lane (warp-uniform state); one
+  // elected lane issues the copies.  Units are slab-local: unit u = (panel p,
+  // local superstep u - p Sk); the weights of panel p start S supersteps apart.
   int c_l = 0, c_ph = -1, islot = 0;
   uint32_t c_u = 0, c_hi = 0, c_segend = 0, c_sk = 0, c_jump = 0;
   bool c_done = false;
@@ -281,9 +288,14 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     const uint32_t nss = min((uint32_t)sss, min(c_hi, c_segend) - c_u);
     unsigned char* dst = ring + (size_t)islot * slot_bytes;
     uint64_t* bar = &full[islot];
-    mbar_expect_tx(bar, nss * (WB + ZB));
-    bulk_g2s(dst, c_w, nss * WB, bar);
-    bulk_g2s(dst + sss * WB, c_z, nss * ZB, bar);
+    if (lane == 0) {
+      // (the slot's last readers are behind a __syncwarp: order their generic
+      // reads before the async-proxy writes)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, nss * (WB + ZB));
+      bulk_g2s(dst, c_w, nss * WB, bar);
+      bulk_g2s(dst + sss * WB, c_z, nss * ZB, bar);
+    }
     if (++islot == depth) islot = 0;
     c_u += nss;
     c_w += nss * WB;
@@ -296,10 +308,8 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
       c_z += (size_t)c_jump * ZB;
     }
   };
-  if (lane == 0) {
-    next_phase();
-    for (int i = 0; i < depth; ++i) issue_one();
-  }
+  next_phase();
+  for (int i = 0; i < depth; ++i) issue_one();
   __syncwarp();
 
   // ---- trace / waiting ----------------------------------------------------------
@@ -443,10 +453,34 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
     return s;
   };
 
+  // L2 prefetch of this warp's unit range of GEMV phase (l, ph), at most
+  // pl.pf_units[ph] units: issued one phase ahead, so HBM keeps streaming through
+  // the hand-offs between phases and the ring copies of that phase hit L2.
+  auto prefetch_phase = [&](int l, int ph) {
+    if (l >= pl.L || lane != 0) return;
+    const uint32_t* row = ctab + ph * kCrow;
+    const uint32_t Sk = row[35], S = pl.S[ph];
+    // (the ring already holds / has requested the first depth * sss units)
+    uint32_t u = row[warp] + (uint32_t)(depth * sss);
+    const uint32_t hi = min(row[warp + 1], u + pl.pf_units[ph]);
+    if (u >= hi) return;
+    uint32_t p = u / Sk;
+    const char* w = ltab[l * kLtab + ph];
+    const char* z = ltab[l * kLtab + 4 + ph];
+    while (u < hi) {
+      const uint32_t seg_end = min(hi, (p + 1) * Sk), n = seg_end - u;
+      const size_t first = (size_t)p * S + row[34] + (u - p * Sk);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(w + first * WB), "r"(n * WB) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(z + first * ZB), "r"(n * ZB) : "memory");
+      u = seg_end;
+      ++p;
+    }
+  };
+
   // ---- one GEMV phase: consume this warp's unit range ----------------------------
   int wslot = 0;
   uint32_t wph = 0;
-  auto gemv_phase = [&](int ph, uint32_t fl, int bs) {
+  auto gemv_phase = [&](int ph, uint32_t fl, int bs, int nl) {
     const uint32_t* row = ctab + ph * kCrow;
     const uint32_t Sk = row[35];
     const uint32_t lo = row[warp], hi = row[warp + 1];
@@ -466,15 +500,15 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
             uint4 w[BITS];
 #pragma unroll
             for (int v = 0; v < BITS; ++v) w[v] = ((const uint4*)(stg + j * WB))[v * 32 + lane];
-            stack_superstep<BITS, GPS>(w, (const float2*)(stg + sss * WB + j * ZB),
-                                       xrec + (size_t)(s + j) * kSRec, yv);
+            if (pl.mode != 1)
+              stack_superstep<BITS, GPS>(w, (const float2*)(stg + sss * WB + j * ZB),
+                                         xrec + (size_t)(s + j) * kSRec, yv);
+            else
+              yv[0] += __uint_as_float(w[0].x & 1u);
           }
         }
         __syncwarp();
-        if (lane == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_one();
-        }
+        issue_one();
         if (++wslot == depth) {
           wslot = 0;
           wph ^= 1u;
@@ -491,6 +525,9 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
       ++seg;
       ++p;
     }
+    // this warp's range is done: pull the next part of its next range into L2
+    // while the phase drains and the next one's inputs are handed over
+    if (pl.mode != 2) prefetch_phase(ph == 3 ? nl + 1 : nl, (ph + 1) & 3);
     __syncthreads();
     stamp(3);
     // the CTA's partial of every panel it touched: its warps' segments in warp
@@ -844,7 +881,7 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
         __syncthreads();
       }
       stamp(2);
-      gemv_phase(st, fl, bs);
+      gemv_phase(st, fl, bs, l);
       if (st == 0) attention(l, fl, bs);
     }
     // Skew bound for the three buffer sets: this CTA enters layer l + 1 (whose
@@ -907,6 +944,16 @@ struct qigen_decode_stack {
 // depth cap
 static thread_local int g_stack_sss = 2;
 static thread_local int g_stack_depth = 8;
+static thread_local int g_stack_mode = 0;
+// MB of L2 prefetch per phase hand-off ((MB + 1) << 8 in qigen_debug_stack_mode).  Off:
+// measured slower at every size (7B layer 36.4 us -> 37.6 / 38.8 / 39.6 us at 8 / 16 / 40 MB):
+// the extra traffic delays the latency-critical flagged loads of the hand-off.
+static thread_local int g_stack_pf = 0;
+extern "C" int qigen_debug_stack_mode(int mode) {
+  g_stack_mode = mode & 255;
+  if (mode >> 8) g_stack_pf = (mode >> 8) - 1;
+  return QIGEN_OK;
+}
 static thread_local int g_stack_ksl = 2424;  // K slabs wanted for qkv, o, gate|up, down (digits)
 extern "C" int qigen_debug_stack_tuning(int sss, int depth, int ksl) {
   g_stack_sss = sss == 1 ? 1 : 2;
@@ -1042,6 +1089,13 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   QIGEN_CHECK_ARG(fits, QIGEN_ERR_UNSUPPORTED,
                   "decode stack: shape outside the static partition's limits");
   pl.two_words = (uint32_t)two.size();
+  // optional L2 prefetch behind the ring's lookahead, issued by a warp when it
+  // finishes a phase (tuning aid, off by default: see g_stack_pf)
+  for (int ph = 0; ph < 4; ++ph) {
+    const double unit_bytes = e.bits * 512 + (256 / e.group_size) * 128;
+    const double cap = (double)g_stack_pf * 1e6 / ((double)G * kSWarps * unit_bytes);
+    pl.pf_units[ph] = (uint32_t)(cap + 0.5);
+  }
   // shared memory: records | rings | warp partials | red | barriers | tables
   const size_t xrec = std::max<size_t>((size_t)skmax * kSRec, kAttScratch);
   const size_t xrec_al = (xrec + 127) / 128 * 128;
@@ -1136,6 +1190,7 @@ extern "C" int qigen_decode_stack_run(const qigen_decode_stack* s, const float* 
   pl.pos = (int)pos;
   pl.scale = scale;
   pl.trace = g_trace;
+  pl.mode = g_stack_mode;
   cudaStream_t st = (cudaStream_t)stream;
   switch (s->bits * 16 + s->gps) {
 #define QS_CASE(B, G) \

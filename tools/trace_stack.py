@@ -19,6 +19,8 @@ L = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 Lb = _lib.lib()
 if len(sys.argv) > 5:
     Lb.qigen_debug_stack_tuning(int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]))
+import os
+Lb.qigen_debug_stack_mode(int(os.environ.get("STACK_MODE", "0")))  # (pf MB + 1) << 8 | mode
 base, ctx = (D.LLAMA_7B, 512) if name == "7b" else (D.LLAMA_65B, 1024)
 cfg = D.shrink(base, n_layers=L)
 m = D.LlamaTP(cfg, batch=1, max_ctx=ctx + 1, seed=0, stack=True, keep_logits=False)
