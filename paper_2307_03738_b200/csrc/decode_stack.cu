@@ -496,15 +496,12 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
         const unsigned char* stg = ring + (size_t)wslot * slot_bytes;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          if (j < (int)nss) {
+          if (j < (int)nss && pl.mode != 1) {  // (mode 1: the copies alone)
             uint4 w[BITS];
 #pragma unroll
             for (int v = 0; v < BITS; ++v) w[v] = ((const uint4*)(stg + j * WB))[v * 32 + lane];
-            if (pl.mode != 1)
-              stack_superstep<BITS, GPS>(w, (const float2*)(stg + sss * WB + j * ZB),
-                                         xrec + (size_t)(s + j) * kSRec, yv);
-            else
-              yv[0] += __uint_as_float(w[0].x & 1u);
+            stack_superstep<BITS, GPS>(w, (const float2*)(stg + sss * WB + j * ZB),
+                                       xrec + (size_t)(s + j) * kSRec, yv);
           }
         }
         __syncwarp();
