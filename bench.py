@@ -408,6 +408,18 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = STEP_BYTES * world * e2e_steps / e2e_s / 1e9
+    # the reference's own seam, one blocking qgemv(pm, x_host) per matrix:
+    # numpy in, numpy out, a host round trip per call (reported next to the batched form)
+    seam_steps = max(1, min(args.steps, 10))
+    for pm, xh in zip(pms, xs_host):
+        q.qgemv(pm, xh)
+    t0 = time.perf_counter()
+    for _ in range(seam_steps):
+        for pm, xh in zip(pms, xs_host):
+            q.qgemv(pm, xh)
+    seam_s = time.perf_counter() - t0
+    seam_gbs = STEP_BYTES * seam_steps / seam_s / 1e9
+    seam_us = seam_s / (seam_steps * len(pms)) * 1e6
     h2d = sum(K * 4 for _, _, (K, N) in SWEEP)
     d2h = sum(N * 4 for _, _, (K, N) in SWEEP)
     del group, graph, chain_graph
@@ -444,7 +456,9 @@ def run_ours(args):
                          "frac": round(kernel_gbs / peak, 4), "traffic": _traffic()},
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "api": "qgemv_batch(pms, xs_host): gather into pinned memory, grouped launch reading it over PCIe and storing y into a fresh pinned block (zero-copy both ways), sync"},
+                    "api": "qgemv_batch(pms, xs_host): gather into pinned memory, grouped launch reading it over PCIe and storing y into a fresh pinned block (zero-copy both ways), sync",
+                    "seam_gbs": round(seam_gbs, 1), "seam_us_per_call": round(seam_us, 1),
+                    "seam": "the same 36 matrices as 36 blocking qgemv(pm, x_host) calls (numpy in / numpy out, the reference's per-matrix seam)"},
             "gpu_launches": k_ours * args.steps,
             "kernels_per_step": {"ours": k_ours, "all": k_total},
             "clocks": sampler.report(),

@@ -314,6 +314,11 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
 
   // ---- trace / waiting ----------------------------------------------------------
   unsigned int nph = 0;  // phases done (5 per layer)
+  if (pl.trace && tid == 0) {  // trace slot 1 of phase 0: the SM this CTA runs on
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    pl.trace[(size_t)cta * 4 + 1] = smid;
+  }
   auto stamp = [&](int i) {  // trace point i of the current phase
     if (pl.trace && tid == 0) pl.trace[((size_t)nph * G + cta) * 4 + i] = gtime();
   };

@@ -71,16 +71,45 @@ for b in range(nbar):
     pro = (t[b, live, 2] - t0).max() - prev
     loop = (t[b, live, 3] - t0).max() - prev
     work = end.max() - prev
-    tot.setdefault(ph, []).append((work, pro, loop, end.max() - end[live].min()))
+    # per-CTA durations (mean over the CTAs that took part): own previous store -> prologue
+    # done -> loop done -> outputs stored
+    own_prev = (t[b - 1, :, 0] - t0) if b else np.zeros(G)
+    d_pro = (t[b, live, 2] - t0 - own_prev[live]).mean()
+    d_loop = (t[b, live, 3] - t[b, live, 2]).mean()
+    d_tail = (t[b, live, 0] - t[b, live, 3]).mean()
+    tot.setdefault(ph, []).append((work, pro, loop, end.max() - end[live].min(), d_pro, d_loop, d_tail))
     if b < 10 or b >= nbar - 5:
         print(f"L{b // 5} {ph:5s} stored {end[live].min():8.2f}-{end.max():8.2f}  phase {work:6.2f}  "
               f"prologue {pro:5.2f}  loop done {loop:5.2f}")
     prev = end.max()
-print("mean per phase (us, since the previous phase's last store): phase, prologue done, loop done, "
-      "spread of the stores")
+print("mean per phase (us): since the previous phase's LAST store: phase, prologue done, loop done; "
+      "spread of the stores; per-CTA means: prologue (own previous store -> records ready), "
+      "loop, tail (loop done -> outputs stored)")
 s_all = 0.0
 for ph in names:
     a = np.array(tot[ph])
     s_all += a[:, 0].mean()
-    print(f"  {ph:5s} {a[:, 0].mean():6.2f} {a[:, 1].mean():6.2f} {a[:, 2].mean():6.2f} {a[:, 3].mean():5.2f}")
+    print(f"  {ph:5s} {a[:, 0].mean():6.2f} {a[:, 1].mean():6.2f} {a[:, 2].mean():6.2f} {a[:, 3].mean():5.2f}"
+          f"   | {a[:, 4].mean():5.2f} {a[:, 5].mean():5.2f} {a[:, 6].mean():5.2f}")
 print(f"  layer total {s_all:.2f} us")
+if os.environ.get("PER_CTA"):
+    # which CTAs finish the gate|up / qkv loops late: the same ones every layer?
+    for name_, b0 in (("gu", 3), ("qkv", 0), ("down", 4)):
+        endl = np.stack([t[b, :, 3] - t[b, :, 3].min() for b in range(b0, nbar, 5)])  # [layers, G]
+        m = endl.mean(0)
+        order = np.argsort(m)
+        print(f"{name_}: loop-done lateness per CTA (us, mean over layers): min {m.min():.2f} "
+              f"p50 {np.median(m):.2f} p90 {np.percentile(m, 90):.2f} max {m.max():.2f}; "
+              f"std over layers (mean over CTAs) {endl.std(0).mean():.2f}")
+        print("  latest CTAs:", [(int(c), round(float(m[c]), 2)) for c in order[-10:]])
+        print("  earliest CTAs:", [(int(c), round(float(m[c]), 2)) for c in order[:10]])
+        grp = [round(float(m[k * (G // 4):(k + 1) * (G // 4)].mean()), 2) for k in range(4)]
+        print("  mean by quarter of the grid:", grp)
+        smid = buf.cpu().numpy().reshape(nbar, G, 4)[0, :, 1]
+        by = {}
+        for c in range(G):
+            by.setdefault(int(smid[c]) // 2 % 8 if False else int(smid[c]) // 20, []).append(m[c])
+        print("  smid of CTA 0..7:", smid[:8].tolist(), " max smid", int(smid.max()))
+        print("  mean lateness by smid // 20:", {k: round(float(np.mean(v)), 2) for k, v in sorted(by.items())})
+        late = order[-12:]
+        print("  smids of the latest CTAs:", sorted(int(smid[c]) for c in late))
