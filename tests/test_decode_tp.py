@@ -330,6 +330,32 @@ def test_decode_stack_matches_per_op_chain(case):
 
 
 @pytest.mark.gpu
+def test_decode_stack_many_layers_many_steps():
+    """Seven layers (the three flagged buffer sets wrap twice) and twelve
+    consecutive greedy steps from position 0 (the launch epoch advances every
+    step; the KV cache fills from empty): the stack generates the same tokens as
+    the per-op chain and the caches end up equal."""
+    cfg = D.LlamaConfig(n_layers=7, d_model=512, n_heads=4, head_dim=128, ffn=1536, vocab=3000,
+                        bits=4, group=64)
+    ref = D.LlamaTP(cfg, batch=1, max_ctx=16, seed=21, device="cuda", stack=False)
+    m = D.LlamaTP(cfg, batch=1, max_ctx=16, seed=21, device="cuda", stack=True)
+    assert m.stack is not None, m.stack_reason
+    # start from an empty cache in both models
+    for mm in (ref, m):
+        mm.k_cache.zero_()
+        mm.v_cache.zero_()
+    t1 = t2 = torch.tensor([123], device="cuda")
+    for p in range(12):
+        t1, t2 = ref.step(t1, p), m.step(t2, p)
+        l1, l2 = ref.last_logits.double(), m.last_logits.double()
+        assert ((l2 - l1).abs().max() / (1 + l1.abs().max())).item() < 5e-4, p
+        assert torch.equal(t1, t2), p
+    assert torch.allclose(m.k_cache[:, :, :, :12].float(), ref.k_cache[:, :, :, :12].float(),
+                          atol=2e-3, rtol=2e-3)
+    assert m.stack_error() == 0
+
+
+@pytest.mark.gpu
 def test_decode_stack_in_a_cuda_graph():
     """The persistent kernel (cooperative launch) is graph-capturable and
     replays give the eager result."""
