@@ -21,9 +21,11 @@ ap.add_argument("--graph", action="store_true")
 ap.add_argument("--group", action="store_true", help="the R copies as one GemvGroup launch (tokens <= 2)")
 ap.add_argument("--gmode", type=lambda v: int(v, 0), default=0, help="qigen_debug_group_mode (1: stream only)")
 ap.add_argument("--x-ready", action="store_true", help="independent GEMVs (QIGEN_GEMV_X_READY)")
+ap.add_argument("--wpc", type=int, default=8, help="qigen_debug_gemv_tuning: warps per CTA (8 or 16)")
 args = ap.parse_args()
 dev = torch.device("cuda")
 q._lib.lib().qigen_debug_group_mode(args.gmode)
+q._lib.lib().qigen_debug_gemv_tuning(0, args.wpc, 0, 0)
 res = []
 for shp in args.shapes.split(","):
     K, N = map(int, shp.split("x"))
