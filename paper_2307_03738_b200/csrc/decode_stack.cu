@@ -4,35 +4,39 @@
 // The per-op chain of the decode driver (decode.py) is latency-bound: each of
 // the five kernels of a layer pays its launch boundary, its activation
 // prologue and its split-K tail on the critical path.  Here one
-// CTA per SM stays resident for the whole step:
+// CTA (16 warps) per SM stays resident for the whole step (cooperative launch):
 //   * the four quantized linears of every layer (fused QKV, o_proj, fused
 //     gate|up, down_proj; same arithmetic as gemv.cu / gemv_grouped.cu: the
 //     reference factorisation kernelgen.py:227-240 with exact IMMA partials)
-//     and the attention in between are PHASES separated by a grid barrier (one
-//     global counter, release/acquire);
-//   * the CTAs form ksl groups (K slabs) x G / ksl panel ranges: group k owns
-//     the k-th slab of every phase's K supersteps, and within a group a phase's
-//     (panel, superstep-of-the-slab) units, in panel-major order, are cut into
-//     equal contiguous ranges, one per warp (e.g. 4 x 37 CTAs x 16 warps).  So a
-//     CTA only ever needs 1 / ksl of each activation vector (its prologue work
-//     and its shared-memory records shrink by ksl) and every warp streams its
-//     range through its own ring of TMA bulk-copy stages.  The schedule is static, so a warp's issue cursor simply runs
-//     ahead into the NEXT phases (and layers): weights keep streaming from HBM
-//     while the CTA sits in a barrier or digitises activations, and the rings
-//     never drain;
+//     and the attention in between are PHASES;
+//   * per GEMV phase the CTAs form ksl groups (K slabs) x G / ksl panel ranges:
+//     group k owns the k-th slab of the phase's K supersteps, and within a group
+//     the (panel, superstep-of-the-slab) units, in panel-major order, are cut
+//     into equal contiguous ranges, one per warp (host-built tables).  So a CTA
+//     needs only 1 / ksl of each activation vector (its prologue work and its
+//     shared-memory records shrink by ksl), and every warp streams its range
+//     through its own ring of TMA bulk-copy stages.  The schedule is static, so
+//     a warp's issue cursor simply runs ahead into the NEXT phases (and
+//     layers): the first stages of a phase are in shared memory before its
+//     inputs exist, and the rings never drain;
 //   * a warp's partial sums of a panel are reduced inside the CTA in warp
 //     order and stored as one partial per (CTA, panel) ("slot": 2 per slab, a
 //     panel of a slab spans at most two CTAs); the consumer of the vector adds
 //     the slots in a fixed order.  No atomics: deterministic;
-//   * the consumer side of each phase ("prologue") is computed redundantly by
-//     every CTA straight into shared memory: residual add, RMSNorm weight,
-//     SwiGLU or the attention combine, then the fixed-point digit records of
-//     the CTA's K slab (1152 B per 256 rows).  The 1/rms of an RMSNorm is
-//     applied to the GEMV's OUTPUT by its consumer (the GEMV is linear), from
-//     the per-slab sums of squares the groups publish;
-//   * attention: each head is split over cph CTAs by position; a warp keeps an
-//     online-softmax state over its positions, the CTA combines its warps and
-//     stores one partial per (head, chunk); the o_proj prologue combines them.
+//   * the consumer side of each phase ("prologue") is computed by every CTA
+//     for its slab straight into shared memory: residual add, RMSNorm weight,
+//     SwiGLU or the attention combine, then the fixed-point digit records
+//     (1152 B per 256 rows).  The residual rows of the slab stay in the CTA's
+//     shared memory.  The 1/rms of an RMSNorm is applied to the GEMV's OUTPUT
+//     by its consumer (the GEMV is linear), from the per-slab sums of squares
+//     the groups publish;
+//   * attention: a head's cached positions are split over cph CTAs; a warp
+//     keeps an online-softmax state over its positions, the CTA combines its
+//     warps and stores one partial per (head, chunk); the o_proj prologue
+//     combines them;
+//   * NO grid barrier between phases (1.3-1.7 us each on 148 CTAs): every value
+//     that crosses CTAs travels as an 8-byte {value, flag} pair, polled by its
+//     reader ("flag in data", see below).
 #include <cuda_fp16.h>
 
 #include <algorithm>

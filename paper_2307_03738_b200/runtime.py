@@ -388,6 +388,17 @@ def qgemv(pm, x, sums=None, threads=None, *, out=None, accumulate: bool = False)
             raise ConfigError(f"x has shape {xa.shape}, expected [{pm.n}] or [tokens, {pm.n}]")
         if not np.all(np.isfinite(xa)):
             raise ConfigError("x contains non-finite values")
+        if xa.ndim == 1 and out is None and not accumulate:
+            # one host vector: the zero-copy path of qgemv_batch with a plan kept per
+            # matrix (x gathered into pinned memory that the kernel reads over PCIe, y
+            # stored into a fresh pinned block; no staged H2D / D2H copies)
+            pw = exec_layout(pm)
+            if GemvGroup.supports(pw):
+                b = getattr(pw, "_single", None)
+                if b is None:
+                    b = pw._single = _Batch([pm], _dev.require_cuda())
+                with b.lock:
+                    return _batch_call(b, [xa])[0]
         xt = _dev.to_device(xa, torch.float32)
     else:
         xt = x
