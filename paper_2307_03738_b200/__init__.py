@@ -16,7 +16,7 @@ from .quant import (CodeMatrix, GroupParams, dequantize, dequantize_matrix, quan
 from .packing import (Layout, PackedMatrix, PackError, block_order, extract_codes,
                       lay_out_blocks, morton_index, pack_words, unpack_words)
 from .runtime import (GemvGroup, InputSums, PanelWeights, input_sums, memory_report, qgemv,
-                      qgemv_batch, qgemv_reference)
+                      qgemv_batch, qgemv_batch_inputs, qgemv_reference)
 
 from .weightfile import (BadMagicError, ChecksumError, TruncatedError, VersionError,
                          WeightFileError, load_panels, read_weight_file, write_weight_file)

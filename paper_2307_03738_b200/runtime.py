@@ -508,6 +508,28 @@ _LAST = [None, None]  # (matrix list object, _Batch) of the previous call
 _SHAPE = operator.attrgetter("shape")
 
 
+class PinnedInputs(list):
+    """The activation vectors of one matrix list as numpy views of its page-locked
+    gather buffer (``qgemv_batch_inputs``)."""
+
+    _batch = None
+
+
+def qgemv_batch_inputs(pms) -> "PinnedInputs":
+    """Page-locked input vectors for ``qgemv_batch(pms, .)``: a list of numpy [n_i]
+    views of the matrix list's pinned gather buffer.  Fill them in place (they are
+    ordinary numpy arrays) and pass the list itself to ``qgemv_batch``: the grouped
+    launch then reads them over PCIe directly, with no host-side gather.  The
+    buffer belongs to the matrix list: one caller at a time."""
+    if not pms:
+        raise ConfigError("qgemv_batch needs one activation vector per matrix")
+    with _CACHE_LOCK:
+        b = _lookup_batch(pms)
+    xs = PinnedInputs(b.xh_np[int(a):int(e)] for a, e in zip(b.koff[:-1], b.koff[1:]))
+    xs._batch = b
+    return xs
+
+
 def qgemv_batch(pms, xs):
     """Independent ``qgemv(pm_i, x_i)`` calls for a list of
     matrices, as ONE grouped GPU launch (``GemvGroup``).  ``xs``: per matrix an
@@ -518,12 +540,16 @@ def qgemv_batch(pms, xs):
     that block, so they stay valid across later calls.  Device inputs give
     CUDA tensors.  The grouped plan and staging buffers are cached per matrix
     list (the 8 most recently used lists); concurrent calls from several
-    threads are safe (calls on the same list are serialised)."""
+    threads are safe (calls on the same list are serialised).  Inputs obtained
+    from ``qgemv_batch_inputs(pms)`` (numpy views of the pinned buffer, filled in
+    place) skip the gather."""
     if len(pms) != len(xs) or not pms:
         raise ConfigError("qgemv_batch needs one activation vector per matrix")
     with _CACHE_LOCK:
         b = _lookup_batch(pms)
     with b.lock:
+        if type(xs) is PinnedInputs and xs._batch is b:
+            return _batch_host_run(b)  # the inputs already are the pinned buffer
         return _batch_call(b, xs)
 
 
