@@ -703,6 +703,7 @@ __global__ void __launch_bounds__(kSThreads, 1) decode_stack_kernel(const SPlan 
           }
           m = mb;
         }
+        stamp(1);
         __syncthreads();  // the new token's k, v are in raw
         if (mine && warp == 0) {  // the new token: one more position
           const float4 kn = *(const float4*)(raw + kHD + 4 * lane);

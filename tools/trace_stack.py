@@ -77,6 +77,10 @@ for b in range(nbar):
     d_pro = (t[b, live, 2] - t0 - own_prev[live]).mean()
     d_loop = (t[b, live, 3] - t[b, live, 2]).mean()
     d_tail = (t[b, live, 0] - t[b, live, 3]).mean()
+    if ph == "attn":
+        print(f"    attention detail (per-CTA means, us): q ready -> KV batch done (warp 0) "
+              f"{(t[b, live, 1] - t[b, live, 2]).mean():.2f}, -> CTA sync + new token "
+              f"{(t[b, live, 3] - t[b, live, 1]).mean():.2f}")
     tot.setdefault(ph, []).append((work, pro, loop, end.max() - end[live].min(), d_pro, d_loop, d_tail))
     if b < 10 or b >= nbar - 5:
         print(f"L{b // 5} {ph:5s} stored {end[live].min():8.2f}-{end.max():8.2f}  phase {work:6.2f}  "
