@@ -515,6 +515,24 @@ def measure_decode(workload, B, ctx, layers, steps, warmup, tp_shard=0):
         for _ in range(2):
             model.step(tok, pos)
         stream.synchronize()
+        if world > 1 and getattr(model, "comm", None) is not None:
+            # the push all-reduce over peer memory has only ever been verified with ranks
+            # emulated on one GPU: check it here (no wait timed out, every rank got the same
+            # greedy tokens) and fall back to NCCL otherwise
+            bad = torch.tensor([1 if model.comm.error() else 0], device="cuda")
+            toks = [torch.empty_like(model.next_tokens) for _ in range(world)]
+            dist.all_gather(toks, model.next_tokens.contiguous())
+            if any(not torch.equal(t, toks[0]) for t in toks):
+                bad.fill_(1)
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+            if int(bad.item()):
+                del model
+                torch.cuda.empty_cache()
+                model = D.LlamaTP(cfg, batch=B, max_ctx=ctx + 1, seed=0, tp=tp, comm="nccl")
+                model.comm_kind = "nccl (the push all-reduce failed its check on this box)"
+                for _ in range(2):
+                    model.step(tok, pos)
+                stream.synchronize()
         if world > 1:
             dist.barrier()
         graph = torch.cuda.CUDAGraph(keep_graph=True)

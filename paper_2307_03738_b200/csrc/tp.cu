@@ -33,7 +33,9 @@ __global__ void __launch_bounds__(256) tp_reduce_kernel(char* base, int world, i
     const unsigned target = ((epoch - 1u) * (unsigned)layers + (unsigned)layer + 1u) * (unsigned)d;
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    bool good = true;
+    // (after a timeout every later reduce of the step fails fast instead of
+    // waiting 4 s again)
+    bool good = *(volatile unsigned*)(base + 68) == 0u;
     for (int q = 0; q < world && good; ++q) {
       while ((int)(ld_acquire_sys(&flags[slot * 8 + q]) - target) < 0) {
         unsigned long long t;
