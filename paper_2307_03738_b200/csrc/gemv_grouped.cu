@@ -149,6 +149,78 @@ __device__ __forceinline__ void group_prep_item(const GPlan& pl, const GDesc& d,
   }
 }
 
+// Exponent units of 256 rows (group sizes >= 256 and full-column: ONE flush per
+// superstep in the consumer): 64 items = two warps agree on the exponent and
+// add their sums through shared memory.  Called by whole 256-thread blocks.
+__device__ __forceinline__ void group_prep_item64(const GPlan& pl, const GDesc& d, int it) {
+  __shared__ uint32_t s_max[8];
+  __shared__ int s_lo[8], s_hi[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool live = it < d.KS * 64;
+  const int st = it >> 3, sub = it & 7;
+  const int sup = st >> 3, sl = st & 7;
+  unsigned char* rec = pl.rec + (size_t)(d.rec0 + (live ? sup : 0)) * kRecBytes;
+#pragma unroll
+  for (int tk = 0; tk < kGTP; ++tk) {
+    if (tk >= d.M) {  // padding token (CTA-uniform): zero digits and flush factors
+      if (live) {
+        store_digits((uint32_t*)rec, sl, tk, kGTP, sub, Digits{{0u, 0u, 0u, 0u}, 0.f, 0.f});
+        if ((it % 64) == 0) ((float4*)(rec + kRecDig))[tk] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (live) gload4(d, tk, (int64_t)32 * st + 16 * (sub >> 2) + 4 * (sub & 3), v);
+    const float m4 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+    const uint32_t wmx = __reduce_max_sync(0xffffffffu, __float_as_uint(m4));
+    __syncthreads();  // (the previous token's exchange is over)
+    if (lane == 0) s_max[warp] = wmx;
+    __syncthreads();
+    const uint32_t umx = max(s_max[warp & ~1], s_max[warp | 1]);
+    // as digitize<> (gemv_common.cuh) from here on, with the unit = this warp pair
+    const int e = umx ? (int)((umx >> 23) & 0xFF) - 126 : 0;
+    const int k = 30 - e, k1 = k >> 1, k2 = k - k1;
+    const float f1 = __int_as_float((127 + k1) << 23), f2 = __int_as_float((127 + k2) << 23);
+    int mv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mv[i] = __float2int_rn(__fmul_rn(__fmul_rn(v[i], f1), f2));
+    uint32_t tt[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tt[i] = (uint32_t)(mv[i] + 0x808080);
+    const uint32_t lo01 = __byte_perm(tt[0], tt[1], 0x5140), lo23 = __byte_perm(tt[2], tt[3], 0x5140);
+    const uint32_t hi01 = __byte_perm(tt[0], tt[1], 0x7362), hi23 = __byte_perm(tt[2], tt[3], 0x7362);
+    Digits dg;
+    dg.dw[3] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;
+    dg.dw[2] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;
+    dg.dw[1] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;
+    dg.dw[0] = __byte_perm(hi01, hi23, 0x7632);
+    int slo = 0, shi = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      slo += mv[i] & 0xFFFF;
+      shi += mv[i] >> 16;
+    }
+    slo = __reduce_add_sync(0xffffffffu, slo);
+    shi = __reduce_add_sync(0xffffffffu, shi);
+    if (lane == 0) {
+      s_lo[warp] = slo;
+      s_hi[warp] = shi;
+    }
+    __syncthreads();
+    slo = s_lo[warp & ~1] + s_lo[warp | 1];
+    shi = s_hi[warp & ~1] + s_hi[warp | 1];
+    dg.xsum = fmaf((float)shi, 65536.f, (float)slo);
+    dg.scale = umx ? __int_as_float((127 + e - 30) << 23) : 0.f;
+    if (umx && e - 30 < -126) dg.scale = scalbnf(1.f, e - 30);
+    if (live) {
+      store_digits((uint32_t*)rec, sl, tk, kGTP, sub, dg);
+      if ((it % 64) == 0)
+        ((float4*)(rec + kRecDig))[tk] =
+            make_float4(dg.scale * 65536.f, dg.xsum * dg.scale, dg.scale, 0.f);
+    }
+  }
+}
+
 // Activation records of every GEMV of the group; grid (ceil(max KS*64/256),
 // count), launched just before the grouped kernel (which prefetches weights
 // meanwhile and waits for it before reading records or claiming items).
@@ -171,10 +243,11 @@ __global__ void __launch_bounds__(256) group_prep_kernel(const GPlan pl) {
       ((float*)((char*)d.y + pl.ydelta))[(i / d.m) * d.ldy + i % d.m] = 0.f;
   if ((int)blockIdx.x * 256 >= d.KS * 64) return;
   const int it = blockIdx.x * 256 + threadIdx.x;
-  const int U = d.g == 32 ? 32 : d.g == 64 ? 64 : 128;  // exponent unit (rows)
-  if (U == 32) group_prep_item<8>(pl, d, it);
-  else if (U == 64) group_prep_item<16>(pl, d, it);
-  else group_prep_item<32>(pl, d, it);
+  // exponent unit (rows): the group, 256 for groups of >= 256 rows / full column
+  if (d.g == 32) group_prep_item<8>(pl, d, it);
+  else if (d.g == 64) group_prep_item<16>(pl, d, it);
+  else if (d.g == 128) group_prep_item<32>(pl, d, it);
+  else group_prep_item64(pl, d, it);
 }
 
 // IMMA with a zero accumulator input (first step of a chain in a unit).
@@ -194,7 +267,10 @@ __device__ __forceinline__ void imma0(int (&c)[4], const uint32_t (&a)[4], uint2
 template <int BITS, int GPS>
 __device__ __forceinline__ void group_superstep(const uint4 (&w)[BITS], const float2* szs,
                                                 const unsigned char* rec, float (&yv)[2]) {
-  constexpr int UPS = GPS > 2 ? GPS : 2;
+  // exponent units per superstep: the groups, one for groups of >= 256 rows / full
+  // column (the digit-pair partial c * 256 + c' of 256 rows still fits an int32:
+  // |c| <= 256 * 240 * 128, see the flush)
+  constexpr int UPS = GPS >= 2 ? GPS : 1;
   constexpr int SPU = 8 / UPS;
   const int lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
   const uint2* bs = (const uint2*)rec + (gq >> 2) * 16 + (gq & 3) * 4 + t;
@@ -644,7 +720,7 @@ extern "C" int qigen_gemv_group_create(int count, const qigen_gemv_desc* descs,
   // instr/ns); ~110 warp instructions per panel superstep + ~17 per flush unit
   auto item_cost = [](const GDesc& d, int act, int nks) {
     const int zb = (d.gps > 0 ? d.gps : 1) * 128;
-    const int ups = d.gps > 2 ? d.gps : 2;
+    const int ups = d.gps >= 2 ? d.gps : 1;
     const double bytes = (double)nks * (act * (d.bits * 512 + zb) + kRecBytes);
     const double instr = (double)nks * act * (110.0 + 17.0 * ups);
     return std::max(bytes / 44.0, instr / 4.5);
