@@ -43,11 +43,16 @@ typedef enum { QIGEN_F32 = 0, QIGEN_F16 = 1, QIGEN_BF16 = 2 } qigen_dtype;
 
 /* Flags for the `accumulate` argument of the GEMV entry points (bit set). */
 #define QIGEN_GEMV_ACCUMULATE 1 /* y += x W instead of y = x W */
-/* x is not written by the kernel launched just before this one on the stream
- * (e.g. independent GEMVs back to back): the GEMV reads and digitises x before
- * its programmatic-dependent-launch wait and waits only before writing y, so it
- * overlaps its predecessor completely.  Never set it when x is the previous
- * kernel's output. */
+/* x is final before this launch (e.g. independent GEMVs back to back on inputs
+ * prepared earlier): the GEMV reads and digitises x before its
+ * programmatic-dependent-launch wait and waits only before writing y, so it
+ * overlaps its predecessor completely; such a GEMV also lets ITS successor start
+ * early.  So x must not be written by ANY kernel that may still be in flight
+ * in the chain of early-starting launches before it, not just by the kernel
+ * launched immediately before: G1 (writes h), G2 (X_READY, independent), G3
+ * (X_READY, x = h) is wrong, because G3 can read h before G1 has written it.
+ * Never set it when x is produced by a kernel of the same stream that was
+ * launched after the last launch without this flag. */
 #define QIGEN_GEMV_X_READY 2
 
 int qigen_version(void);
