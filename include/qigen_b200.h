@@ -413,9 +413,11 @@ int qigen_decode_stack_destroy(qigen_decode_stack* s);
  * (1 or 2), the cap on ring stages per warp and the K slabs (1, 2 or 4) wanted for
  * the qkv, o, gate|up and down phases as four digits (default 2424). */
 int qigen_debug_stack_tuning(int sss, int depth, int ksl);
-/* Tuning aid (per calling thread): low byte, read at run: 1 = stream the weights
+/* Tuning aid (per calling thread): bits 0-1, read at run: 1 = stream the weights
  * through the rings without the math (results are meaningless): the data-movement
- * floor; bits 8+, read at create: (MB + 1) of L2 prefetch per phase hand-off. */
+ * floor; bits 2-4, read at create: cap on the position chunks (CTAs) per head of
+ * the attention phase (0 = default 4); bits 8+, read at create: (MB + 1) of L2
+ * prefetch per phase hand-off. */
 int qigen_debug_stack_mode(int mode);
 
 /* ---- owning handle (for C callers; the Python host uses the calls above) ---- */

@@ -952,12 +952,14 @@ struct qigen_decode_stack {
 static thread_local int g_stack_sss = 2;
 static thread_local int g_stack_depth = 8;
 static thread_local int g_stack_mode = 0;
+static thread_local int g_stack_cph = kMaxCph;  // cap on the position chunks (CTAs) per head
 // MB of L2 prefetch per phase hand-off ((MB + 1) << 8 in qigen_debug_stack_mode).  Off:
 // measured slower at every size (7B layer 36.4 us -> 37.6 / 38.8 / 39.6 us at 8 / 16 / 40 MB):
 // the extra traffic delays the latency-critical flagged loads of the hand-off.
 static thread_local int g_stack_pf = 0;
 extern "C" int qigen_debug_stack_mode(int mode) {
-  g_stack_mode = mode & 255;
+  g_stack_mode = mode & 3;
+  g_stack_cph = (mode >> 2) & 7 ? std::min(kMaxCph, (mode >> 2) & 7) : kMaxCph;
   if (mode >> 8) g_stack_pf = (mode >> 8) - 1;
   return QIGEN_OK;
 }
@@ -1038,7 +1040,7 @@ extern "C" int qigen_decode_stack_create(const qigen_stack_desc* desc,
   pl.ctx = (int)e.ctx;
   pl.G = G;
   pl.eps = e.eps;
-  pl.cph = std::max(1, std::min(kMaxCph, G / e.heads));
+  pl.cph = std::max(1, std::min(g_stack_cph, G / e.heads));
   // per-CTA unit ranges and the two-CTA panel bits of the static partition
   std::vector<uint32_t> ctab((size_t)G * kCtab, 0u), two;
   uint32_t skmax = 0;
