@@ -356,6 +356,26 @@ def test_decode_stack_many_layers_many_steps():
 
 
 @pytest.mark.gpu
+def test_decode_stack_writes_only_the_new_kv_row():
+    """Out-of-bounds check for the persistent kernel (compute-sanitizer is closed on the
+    pool): after a step at position p the KV caches differ from their previous contents in
+    row p only, for every layer and head, and the row after the caches' last position (a
+    guard row of the allocation) is untouched."""
+    cfg, ctx, pos = STACK_CASES["d1024_b3g64"]
+    m = D.LlamaTP(cfg, batch=1, max_ctx=ctx, seed=13, device="cuda", stack=True)
+    assert m.stack is not None, m.stack_reason
+    k0, v0 = m.k_cache.clone(), m.v_cache.clone()
+    m.step(torch.tensor([9], device="cuda"), pos)
+    torch.cuda.synchronize()
+    keep = torch.ones(ctx, dtype=torch.bool, device="cuda")
+    keep[pos] = False
+    assert torch.equal(m.k_cache[:, :, :, keep], k0[:, :, :, keep])
+    assert torch.equal(m.v_cache[:, :, :, keep], v0[:, :, :, keep])
+    assert not torch.equal(m.k_cache[:, :, :, pos], k0[:, :, :, pos])
+    assert m.stack_error() == 0
+
+
+@pytest.mark.gpu
 def test_decode_stack_in_a_cuda_graph():
     """The persistent kernel (cooperative launch) is graph-capturable and
     replays give the eager result."""
