@@ -359,8 +359,7 @@ def test_decode_stack_many_layers_many_steps():
 def test_decode_stack_writes_only_the_new_kv_row():
     """Out-of-bounds check for the persistent kernel (compute-sanitizer is closed on the
     pool): after a step at position p the KV caches differ from their previous contents in
-    row p only, for every layer and head, and the row after the caches' last position (a
-    guard row of the allocation) is untouched."""
+    row p only, for every layer and head."""
     cfg, ctx, pos = STACK_CASES["d1024_b3g64"]
     m = D.LlamaTP(cfg, batch=1, max_ctx=ctx, seed=13, device="cuda", stack=True)
     assert m.stack is not None, m.stack_reason
